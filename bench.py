@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark of the integral-image scatterplot regularizer (BASELINE.json metric:
+"regularization iters/sec (1M pts, 1024^2 grid); integral-image GB/s vs HBM peak").
+
+Workload (BASELINE.json configs[1], the paper's Fig. 5 case): 1,000,000 points in
+four Gaussian clusters (400k/300k/200k/100k, sigma 0.05, centres at 0.3/0.7),
+float32-representable, on a 1024^2 grid, kernel_size 8, 10 iterations.  One "step" is
+one full 10-iteration regularization of that input, device resident (inputs already in
+HBM).  L2 is flushed (256 MiB write) between timed steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun (N > 1) every rank regularizes its own plot (a SPLOM shard, weak
+scaling) and the final positions are all-gathered over NCCL inside the step; the
+step time is the max over ranks.
+
+`--impl reference` times the reference algorithm's CPU implementation (the C port in
+oracle/, all host threads) on the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_POINTS = 1_000_000
+K_GRID = 10
+KERNEL_SIZE = 8
+ITERS = 10
+METRIC = "regularization iters/sec (1M pts, 1024² grid); integral-image GB/s vs HBM peak"
+
+
+def four_cluster(n: int = N_POINTS, seed: int = 4) -> np.ndarray:
+    """Four Gaussian clusters (0.4/0.3/0.2/0.1 of n, sigma 0.05, centres 0.3/0.7),
+    resampled until inside [0,1]^2, rounded to float32-representable values."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    centres = ((0.3, 0.3), (0.7, 0.3), (0.3, 0.7), (0.7, 0.7))
+    counts = [n * 4 // 10, n * 3 // 10, n * 2 // 10]
+    counts.append(n - sum(counts))
+    parts = []
+    for c, m in zip(centres, counts):
+        p = rng.normal(c, 0.05, size=(m, 2))
+        for _ in range(64):
+            bad = np.any((p < 0) | (p > 1), axis=1)
+            if not bad.any():
+                break
+            p[bad] = rng.normal(c, 0.05, size=(int(bad.sum()), 2))
+        parts.append(np.clip(p, 0, 1))
+    return np.concatenate(parts).astype(np.float32).astype(np.float64)
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler(threading.Thread):
+    """Samples SM clock and throttle reasons through NVML during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.005):
+        super().__init__(daemon=True)
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.stop_flag = threading.Event()
+        self.max_mhz = None
+        self.ok = False
+
+    def run(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+                "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+            }
+            self.ok = True
+            while not self.stop_flag.is_set():
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for nm, bit in names.items():
+                    if r & bit and nm != "gpu_idle":
+                        self.reasons.add(nm)
+                time.sleep(self.period)
+        except Exception as e:  # NVML missing: report it rather than inventing clocks
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+
+    def summary(self):
+        self.stop_flag.set()
+        self.join(timeout=2)
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# Algorithmic bytes per launch of each kernel,
+# n points, m = s^2 pixels.
+def algorithmic_bytes(name: str, n: int, m: int) -> int:
+    table = {
+        "splat": 8 * n + 4 * m,            # read fp32 (x,y); counts written once
+        "smooth_h": 4 * m + 4 * m,         # read counts, write the horizontal pass
+        "smooth_v_reduce": 4 * m + 4 * m,  # read the horizontal pass, write d
+        "write_field": 4 * m + 8 * m,      # read d, write the (s,s,2) field
+        "sample": 16 * n + 8 * m,          # read + write fp32 points, field gathered once
+        "memset_counts": 4 * m,
+    }
+    return table.get(name, 0)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world: int, backend: str):
+    import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return dist
+
+
+# ------------------------------------------------------------------------ our arm
+def bench_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    import paper_2408_06513_b200 as P
+    from paper_2408_06513_b200 import _device as D
+    from paper_2408_06513_b200 import _lib
+
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    host = four_cluster(N_POINTS, seed=4 + rank)
+    n, k = len(host), K_GRID
+    m = 1 << (2 * k)
+    pts_in = torch.from_numpy(host.astype(np.float32)).to(dev)
+    pts = torch.empty_like(pts_in)
+    ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    gathered = torch.empty((world, n, 2), dtype=torch.float32, device=dev) if world > 1 else None
+    stream = D.stream()
+
+    def step():
+        pts.copy_(pts_in)
+        _lib.check(lib.inim_run(D.ptr(pts), n, k, KERNEL_SIZE, 0.0, ITERS, 0.0, None, None, None, None, None,
+                                D.ptr(ws), stream), "inim_run")
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered, pts)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for q in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2), outside the step events
+        starts[q].record()
+        step()
+        ends[q].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.summary()
+    t_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if world > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    value = world * ITERS * args.steps / (t_ms / 1e3)
+
+    # -- per-kernel attribution: eager launches with an event after each launch
+    cap = 64 * ITERS
+    ms = (ctypes.c_float * cap)()
+    names = ctypes.create_string_buffer(cap * 24)
+    per_kernel: dict = {}
+    prof_steps = 3
+    for _ in range(prof_steps):
+        flush.zero_()
+        pts.copy_(pts_in)
+        cnt = lib.inim_profile_run(D.ptr(pts), n, k, KERNEL_SIZE, 0.0, ITERS, D.ptr(ws), stream, ms, cap, names,
+                                   len(names))
+        if cnt < 0:
+            _lib.check(cnt, "profile_run")
+        for nm, v in zip(names.value.decode().split("\n")[:cnt], ms[:cnt]):
+            e = per_kernel.setdefault(nm, [0.0, 0])
+            e[0] += v
+            e[1] += 1
+    prof_total = sum(v[0] for v in per_kernel.values()) / prof_steps
+    kernels = {nm: {"avg_us": 1e3 * v[0] / v[1], "launches_per_step": v[1] // prof_steps,
+                    "share": (v[0] / prof_steps) / prof_total} for nm, v in per_kernel.items()}
+    dom = max((nm for nm in kernels if nm != "memset_counts"), key=lambda nm: kernels[nm]["share"])
+    peaks = measured_peaks()
+    dom_bytes = algorithmic_bytes(dom, n, m)
+    achieved = dom_bytes / (kernels[dom]["avg_us"] * 1e-6) / 1e9 if dom_bytes else None
+
+    # -- integral-image pass alone (BASELINE configs[4] at 4096^2), L2 flushed between reps
+    integral = bench_integral(lib, D, dev, flush, sizes=(12,), reps=10)
+
+    # -- end to end through the public API with host buffers (pinned), rank-local
+    e2e = bench_e2e(P, host, reps=max(3, min(args.steps, 10)))
+
+    if rank != 0:
+        return
+    cpu = cpu_baseline(host) if world == 1 and not args.no_cpu_baseline else None
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "iters/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic four-cluster (400k/300k/200k/100k, sigma 0.05), fp32-representable",
+        "config": {"workload": "1M pts, 1024^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[1])",
+                   "points": n, "grid": 1 << k, "iterations_per_step": ITERS, "kernel_size": KERNEL_SIZE,
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": f"splom-shard x{world}" if world > 1 else "single plot"},
+        "e2e": e2e,
+        "gpu_launches": int(args.steps * ITERS * lib.inim_kernels_per_iteration(k)),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": kernels[dom]["avg_us"],
+                     "peak_source": peaks["source"],
+                     "method": "per-launch CUDA events on the launch stream (eager replay of the timed step)"},
+        "kernels": kernels,
+        "integral_image": integral,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_integral(lib, D, dev, flush, sizes=(12,), reps=10):
+    """inim_integral_set GB/s on random fp32 textures, 36 B/px algorithmic."""
+    import torch
+    from paper_2408_06513_b200 import _lib
+
+    peaks = measured_peaks()
+    out = []
+    for k in sizes:
+        s = 1 << k
+        g = torch.Generator(device=dev)
+        g.manual_seed(1234)
+        d = torch.rand((s, s), generator=g, device=dev, dtype=torch.float32) * 10.0
+        tables = torch.empty((8, s, s), dtype=torch.float32, device=dev)
+        total = torch.empty(1, dtype=torch.float64, device=dev)
+        ws = torch.empty(int(lib.inim_workspace_bytes(k, 0)), dtype=torch.uint8, device=dev)
+        st = D.stream()
+
+        def once():
+            _lib.check(lib.inim_integral_set(D.ptr(d), k, D.ptr(tables), D.ptr(total), D.ptr(ws), st), "integral")
+
+        for _ in range(3):
+            once()
+        times = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            once()
+            b.record()
+            b.synchronize()
+            times.append(a.elapsed_time(b))
+        t = statistics.median(times) / 1e3
+        gbs = 36 * s * s / t / 1e9
+        out.append({"size": s, "ms": t * 1e3, "GB_s": gbs, "frac": gbs / peaks["hbm_gbs"],
+                    "bytes_per_px": 36, "l2": "flushed"})
+        del d, tables, ws
+    return out
+
+
+def bench_e2e(P, host: np.ndarray, reps: int):
+    """Same metric through the public drop-in API with host (pinned) buffers: H2D of the
+    float64 positions, 10 device iterations, D2H of the final frame, every call."""
+    import torch
+
+    n = len(host)
+    pinned = torch.empty((n, 2), dtype=torch.float64).pin_memory()
+    pinned.numpy()[:] = host
+    pos = pinned.numpy()
+    params = P.RegularizationParams(k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS, frame_cap=2)
+
+    def call():
+        r = P.run(P.ScatterDataset(positions=pos), params, store_fields=False)
+        return r.frame(ITERS)
+
+    for _ in range(2):
+        call()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        out = call()
+    dt = (time.perf_counter() - t0) / reps
+    assert out.shape == (n, 2)
+    return {"value": ITERS / dt, "unit": "iters/s", "h2d_bytes_per_step": int(n * 2 * 8),
+            "d2h_bytes_per_step": int(n * 2 * 8), "ms_per_call": dt * 1e3,
+            "api": "paper_2408_06513_b200.run(ScatterDataset, RegularizationParams(k=10, kernel_size=8, "
+                   "iterations=10, frame_cap=2), store_fields=False).frame(10)"}
+
+
+# ------------------------------------------------------------------ CPU baseline
+def cpu_baseline(host: np.ndarray, iterations: int = 4):
+    """The oracle (C restatement of the reference algorithm, float64) with every host
+    thread, on a bounded sample: `iterations` iterations of the same 1M / 1024^2 input."""
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    defect = O.flat_response(K_GRID)
+    pos = host
+    t0 = time.perf_counter()
+    for _ in range(iterations):
+        pos = O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
+    dt = time.perf_counter() - t0
+    return {"value": iterations / dt, "unit": "iters/s", "cores": cores, "kind": "port",
+            "sample": f"{iterations} iterations of the 1M-point / 1024^2 / ks=8 workload (float64 C port of "
+                      f"the reference algorithm, OpenMP {cores} threads)"}
+
+
+def bench_reference(args):
+    rank, world, _local = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    host = four_cluster(N_POINTS, seed=4)
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    defect = O.flat_response(K_GRID)
+    pos = host
+    for _ in range(args.warmup):
+        pos = O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
+    pos = host
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        pos = O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    sample = (f"each step = 1 iteration of the 1M-point / 1024^2 / ks=8 workload (the timed unit of our arm is "
+              f"10 iterations); float64 C port of the reference algorithm, OpenMP {cores} threads")
+    line = {
+        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic four-cluster, fp32-representable",
+        "config": {"workload": "1M pts, 1024^2 grid, kernel_size 8 (BASELINE configs[1])", "points": len(host),
+                   "grid": 1 << K_GRID},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+    _rank, world, _ = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

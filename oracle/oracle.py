@@ -1,0 +1,231 @@
+"""ctypes front end of the CPU parity oracle (TEST INFRASTRUCTURE ONLY).
+
+Wraps ``oracle/liboracle.so`` (built from ``inim_oracle.c`` by ``oracle/Makefile``), a
+float64 restatement of the reference hot path (``uncrowd``: density.py, integral.py,
+mapping.py, regularize.py).  Every function below names the reference symbol it
+restates.  Only tests, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline /
+``--impl reference`` leg import this module; the product package never does.
+
+Pinned against golden vectors recorded from the real reference
+(tests/golden/make_golden.py -> tests/golden/*.npz; checked by
+tests/test_oracle_golden.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "liboracle.so"
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64 = ctypes.c_int64
+
+
+def build(force: bool = False) -> Path:
+    """Compile the C restatement (``make -C oracle``)."""
+    src = _HERE / "inim_oracle.c"
+    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(str(_LIB_PATH))
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_threads.restype = ctypes.c_int
+        L.orc_accumulate.argtypes = [_dp, _i64, ctypes.c_int, _dp]
+        L.orc_smoothing_kernel.argtypes = [ctypes.c_int, _dp]
+        L.orc_gaussian_smooth.argtypes = [_dp, _i64, ctypes.c_int, _dp]
+        L.orc_build_density.argtypes = [_dp, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_double, _dp, _dp]
+        L.orc_column_integrals.argtypes = [_dp, _i64, _dp, _dp]
+        L.orc_build_integral_set.argtypes = [_dp, _i64, _dp, _dp]
+        L.orc_raw_targets_per_pixel.argtypes = [_dp, ctypes.c_double, ctypes.c_int, _dp]
+        L.orc_flat_response.argtypes = [ctypes.c_int, _dp]
+        L.orc_build_field.argtypes = [_dp, ctypes.c_double, ctypes.c_int, _dp, _dp, _dp]
+        L.orc_sample_field.argtypes = [_dp, ctypes.c_int, _dp, _i64, _dp]
+        L.orc_iterate_once.argtypes = [_dp, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                       _dp, _dp, _dp, _dp, _dp]
+        L.orc_sum.argtypes = [_dp, _i64]
+        L.orc_sum.restype = ctypes.c_double
+        _lib = L
+        threads = int(os.environ.get("INIM_ORACLE_THREADS", "0"))
+        if threads > 0:
+            L.orc_set_threads(threads)
+    return _lib
+
+
+def set_threads(n: int) -> int:
+    return lib().orc_set_threads(int(n))
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _check(rc: int, what: str):
+    if rc == 1:
+        raise ValueError(f"oracle {what}: invalid argument")
+    if rc == 2:
+        raise MemoryError(f"oracle {what}: out of memory")
+    if rc == 3:
+        raise ValueError(f"oracle {what}: total texture mass must be > 0")
+    if rc:
+        raise RuntimeError(f"oracle {what}: error {rc}")
+
+
+def accumulate(positions, k: int) -> np.ndarray:
+    """density.accumulate (density.py:14-27)."""
+    pos = _f64(positions).reshape(-1, 2)
+    s = 1 << k
+    grid = np.empty((s, s))
+    _check(lib().orc_accumulate(_p(pos), len(pos), k, _p(grid)), "accumulate")
+    return grid
+
+
+def smoothing_kernel(kernel_size: int) -> np.ndarray:
+    """density.smoothing_kernel (density.py:30-37)."""
+    w = np.empty(6 * kernel_size + 1)
+    _check(lib().orc_smoothing_kernel(kernel_size, _p(w)), "smoothing_kernel")
+    return w
+
+
+def gaussian_smooth(grid, kernel_size: int) -> np.ndarray:
+    """density.gaussian_smooth (density.py:40-51)."""
+    g = _f64(grid)
+    out = np.empty_like(g)
+    _check(lib().orc_gaussian_smooth(_p(g), g.shape[0], kernel_size, _p(out)), "gaussian_smooth")
+    return out
+
+
+def build_density(positions, k: int, kernel_size: int, background=None):
+    """density.build_density (density.py:54-78) -> (values, background)."""
+    pos = _f64(positions).reshape(-1, 2)
+    s = 1 << k
+    values = np.empty((s, s))
+    bg = ctypes.c_double(0.0)
+    b = -1.0 if background is None else float(background)
+    _check(lib().orc_build_density(_p(pos), len(pos), k, kernel_size, b, _p(values), ctypes.byref(bg)),
+           "build_density")
+    return values, bg.value
+
+
+def column_integrals(d):
+    """integral.column_integrals (integral.py:180-186) -> (upper, lower)."""
+    d = _f64(d)
+    upper = np.empty_like(d)
+    lower = np.empty_like(d)
+    _check(lib().orc_column_integrals(_p(d), d.shape[0], _p(upper), _p(lower)), "column_integrals")
+    return upper, lower
+
+
+def build_integral_set(d):
+    """integral.build_integral_set (integral.py:231-247) -> (tables[8,s,s], total)."""
+    d = _f64(d)
+    s = d.shape[0]
+    if d.ndim != 2 or d.shape[1] != s or s & (s - 1):
+        raise ValueError("texture must be square with a power-of-two side")
+    t8 = np.empty((8, s, s))
+    total = ctypes.c_double(0.0)
+    _check(lib().orc_build_integral_set(_p(d), s, _p(t8), ctypes.byref(total)), "build_integral_set")
+    return t8, total.value
+
+
+def raw_targets_per_pixel(tables8, total: float, k: int) -> np.ndarray:
+    """mapping._raw_targets_per_pixel (mapping.py:181-191)."""
+    t8 = _f64(tables8)
+    s = 1 << k
+    out = np.empty((s, s, 2))
+    _check(lib().orc_raw_targets_per_pixel(_p(t8), float(total), k, _p(out)), "raw_targets")
+    return out
+
+
+def flat_response(k: int) -> np.ndarray:
+    """mapping.flat_response.get(k) (mapping.py:120-126)."""
+    s = 1 << k
+    out = np.empty((s, s, 2))
+    _check(lib().orc_flat_response(k, _p(out)), "flat_response")
+    return out
+
+
+def build_field(tables8, total: float, k: int, defect=None):
+    """mapping.build_field (mapping.py:194-204) -> (targets, max_excursion)."""
+    t8 = _f64(tables8)
+    if defect is None:
+        defect = flat_response(k)
+    defect = _f64(defect)
+    s = 1 << k
+    out = np.empty((s, s, 2))
+    exc = ctypes.c_double(0.0)
+    _check(lib().orc_build_field(_p(t8), float(total), k, _p(defect), _p(out), ctypes.byref(exc)), "build_field")
+    return out, exc.value
+
+
+def sample_field(targets, points) -> np.ndarray:
+    """mapping.sample_field (mapping.py:207-246)."""
+    t = _f64(targets)
+    k = int(t.shape[0]).bit_length() - 1
+    pts = _f64(points)
+    flat = pts.reshape(-1, 2)
+    out = np.empty_like(flat)
+    _check(lib().orc_sample_field(_p(t), k, _p(flat), len(flat), _p(out)), "sample_field")
+    return out.reshape(pts.shape)
+
+
+def iterate_once(positions, k: int, kernel_size: int, background=None, defect=None,
+                 want_field: bool = False, want_density: bool = False):
+    """regularize.iterate_once (regularize.py:25-37) -> new positions [, field, density]."""
+    pos = _f64(positions).reshape(-1, 2)
+    s = 1 << k
+    new = np.empty_like(pos)
+    field = np.empty((s, s, 2)) if want_field else None
+    dens = np.empty((s, s)) if want_density else None
+    if defect is not None:
+        defect = _f64(defect)
+    b = -1.0 if background is None else float(background)
+    exc = ctypes.c_double(0.0)
+    null = ctypes.cast(None, _dp)
+    _check(lib().orc_iterate_once(_p(pos), len(pos), k, kernel_size, b,
+                                  _p(defect) if defect is not None else null, _p(new),
+                                  _p(field) if field is not None else null,
+                                  _p(dens) if dens is not None else null, ctypes.byref(exc)),
+           "iterate_once")
+    if want_field or want_density:
+        return new, field, dens
+    return new
+
+
+def run_positions(positions, k: int, kernel_size: int, iterations: int, background=None,
+                  stop: str = "fixed", epsilon: float = 1e-4):
+    """regularize.run (regularize.py:40-80) restricted to the numeric path: returns the
+    list of frames [frame0, frame1, ...] (no metrics, no thinning)."""
+    pos = _f64(positions).reshape(-1, 2)
+    defect = flat_response(k)
+    frames = [pos]
+    for _t in range(iterations):
+        new = iterate_once(pos, k, kernel_size, background, defect)
+        frames.append(new)
+        disp = float(np.abs(new - pos).max()) if len(pos) else 0.0
+        pos = new
+        if stop == "displacement" and disp < epsilon:
+            break
+    return frames
+
+
+def total(values) -> float:
+    """float(values.sum()) restated with numpy's pairwise summation (integral.py:246)."""
+    v = _f64(values).ravel()
+    return lib().orc_sum(_p(v), len(v))

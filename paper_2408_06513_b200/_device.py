@@ -1,0 +1,80 @@
+"""Device plumbing: CUDA availability, streams, workspace cache, host<->device moves.
+
+PyTorch only allocates memory and supplies the stream; all arithmetic is in
+libinim.so.  Nothing here computes on the CPU: without a CUDA device the package
+raises instead of falling back.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+_ws_cache: dict = {}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2408_06513_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return _lib.load()
+
+
+def device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> ctypes.c_void_p:
+    if t is None:
+        return ctypes.c_void_p(None)
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def workspace(k: int, n: int = 0) -> torch.Tensor:
+    """Grow-only per-device workspace for a 2^k grid and n points."""
+    lib = require_cuda()
+    need = int(lib.inim_workspace_bytes(int(k), int(n)))
+    if need == 0:
+        raise ValueError(f"k={k} out of range")
+    key = torch.cuda.current_device()
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < need:
+        if ws is not None:
+            torch.cuda.synchronize()
+            lib.inim_clear_graph_cache()
+        ws = torch.empty(need, dtype=torch.uint8, device=device())
+        _ws_cache[key] = ws
+    return ws
+
+
+def to_device(a, dtype=torch.float32) -> torch.Tensor:
+    """Host array (any float dtype) -> contiguous device tensor of `dtype`."""
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device(), dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(a)
+    if dtype == torch.float32:
+        # ship float64 as-is and narrow on the device (one cast kernel)
+        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device(), non_blocking=False)
+        out = torch.empty(src.shape, dtype=torch.float32, device=device())
+        lib = require_cuda()
+        _lib.check(lib.inim_cast_f64_to_f32(ptr(src), ptr(out), src.numel(), stream()), "cast")
+        return out
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device())
+
+
+def to_host64(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> host float64 ndarray (widened on the device)."""
+    if t.dtype == torch.float64:
+        return t.detach().cpu().numpy()
+    lib = require_cuda()
+    t = t.contiguous()
+    out = torch.empty(t.shape, dtype=torch.float64, device=t.device)
+    _lib.check(lib.inim_cast_f32_to_f64(ptr(t), ptr(out), t.numel(), stream()), "cast")
+    return out.cpu().numpy()

@@ -1,0 +1,469 @@
+// C ABI (include/inim.h): argument checks, launch sequencing, the device-resident
+// iteration (regularize.iterate_once / run, reference regularize.py:25-80) and its
+// CUDA-graph replay.
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "inim_internal.cuh"
+
+namespace inim {
+int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st);
+int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cudaStream_t st);
+int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
+                      const int* state, cudaStream_t st);
+int launch_sample_f64(const float* tg, int k, const double* in, double* out, int64_t n, int clip, cudaStream_t st);
+int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_t st);
+int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st);
+int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st);
+int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
+                        float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st);
+int launch_field_from_tables(const float* t8, int k, const double* total, const float* defect, float* targets,
+                             float* max_exc, cudaStream_t st);
+int launch_flat_response(int k, float* defect, cudaStream_t st);
+int launch_line_scan(const float* in, float* out, int s, int dj, int di, int exclusive, cudaStream_t st);
+
+// Per-iteration bookkeeping for the displacement criterion (regularize.py:76-79).
+__global__ void iter_begin_kernel(float* max_exc, float* disp, const int* state) {
+    if (state && state[0]) return;
+    if (max_exc) *max_exc = 0.f;
+    if (disp) *disp = 0.f;
+}
+
+__global__ void iter_end_kernel(const float* disp, float eps, int* state) {
+    if (state[0]) return;
+    state[1] += 1;
+    if (*disp < eps) state[0] = 1;
+}
+
+struct IterBufs {
+    uint32_t* counts;
+    float* d;
+    float* targets;
+    float* scratch;  // >= 4 floats
+    float* pong;     // n*2 floats (run only)
+};
+
+// Workspace = integral layout + grid buffers + point ping-pong.
+struct FullLayout {
+    WsLayout L;
+    size_t counts, d, targets, scratch, pong, bytes;
+};
+
+static FullLayout full_layout(const Geo& g, int64_t n) {
+    FullLayout F;
+    F.L = make_layout(g);
+    size_t o = F.L.bytes;
+    auto take = [&](size_t bytes) {
+        size_t r = o;
+        o = align256(o + bytes);
+        return r;
+    };
+    F.counts = take(sizeof(uint32_t) * g.m);
+    F.d = take(sizeof(float) * g.m);
+    F.targets = take(sizeof(float) * 2 * g.m);
+    F.scratch = take(sizeof(float) * 64);
+    F.pong = take(sizeof(float) * 2 * (size_t)(n > 0 ? n : 1));
+    F.bytes = o;
+    return F;
+}
+
+static bool k_ok(int k) { return k >= 0 && k <= INIM_MAX_K; }
+
+static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, const Geo& g, int kernel_size,
+                             float background, const float* defect, uint32_t* counts, float* d, float* targets,
+                             float* max_exc, float* disp, float stop_eps, int* state, const Ws& ws,
+                             const CUtensorMap* map, cudaStream_t st) {
+    const int* flag = stop_eps > 0.f ? state : nullptr;
+    iter_begin_kernel<<<1, 1, 0, st>>>(max_exc, disp, flag);
+    prof_mark(st, "iter_begin");
+    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * g.m, st));
+    prof_mark(st, "memset_counts");
+    int rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st);
+    if (rc) return rc;
+    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st);
+    if (rc) return rc;
+    rc = launch_carry_scan_state(g, ws, flag, st);
+    if (rc) return rc;
+    rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st);
+    if (rc) return rc;
+    rc = launch_sample_f32(targets, g.k, pts_in, pts_out, n, 1, disp, flag, st);
+    if (rc) return rc;
+    if (flag) {
+        iter_end_kernel<<<1, 1, 0, st>>>(disp, stop_eps, state);
+        prof_mark(st, "iter_end");
+    }
+    return (int)cudaGetLastError();
+}
+
+Prof* g_prof = nullptr;
+
+static float auto_background(int64_t n, int k, float background) {
+    if (background > 0.f) return background;
+    double bg = (double)n / (double)((int64_t)1 << (2 * k));
+    return bg == 0.0 ? 1.0f : (float)bg;
+}
+
+// ---- graph cache for inim_run ---------------------------------------------------------
+struct RunKey {
+    const void* pts;
+    int64_t n;
+    int k, ks;
+    float bg;
+    int iters;
+    float eps;
+    const void *frames, *fields, *disp, *exc, *state, *ws;
+    cudaStream_t st;
+    bool operator==(const RunKey& o) const { return memcmp(this, &o, sizeof(RunKey)) == 0; }
+};
+
+struct RunEntry {
+    RunKey key;
+    cudaGraphExec_t exec;
+};
+
+static std::mutex g_mu;
+static std::vector<RunEntry> g_cache;
+
+static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fields, float* disp, float* excursions,
+                       int* state, void* ws, cudaStream_t st) {
+    const Geo g = make_geo(key.k);
+    const FullLayout F = full_layout(g, key.n);
+    const Ws w = make_ws(ws, F.L);
+    char* base = static_cast<char*>(ws);
+    uint32_t* counts = reinterpret_cast<uint32_t*>(base + F.counts);
+    float* d = reinterpret_cast<float*>(base + F.d);
+    float* tg_scratch = reinterpret_cast<float*>(base + F.targets);
+    float* scratch = reinterpret_cast<float*>(base + F.scratch);
+    float* pong = reinterpret_cast<float*>(base + F.pong);
+    CUtensorMap map;
+    const CUtensorMap* mp = nullptr;
+    if (g.TW >= 32) {
+        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, g.TH);
+        if (rc) return rc;
+        mp = &map;
+    }
+    const size_t pbytes = sizeof(float) * 2 * (size_t)key.n;
+    if (frames && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(frames, pts, pbytes, cudaMemcpyDeviceToDevice, st));
+    float* bufs[2] = {pts, pong};
+    for (int t = 0; t < key.iters; ++t) {
+        float* src = bufs[t & 1];
+        float* dst = bufs[(t + 1) & 1];
+        float* tg = fields ? fields + (size_t)t * 2 * g.m : tg_scratch;
+        float* dsp = disp ? disp + t : scratch;
+        float* ex = excursions ? excursions + t : scratch + 1;
+        int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, nullptr, counts, d, tg, ex, dsp, key.eps, state,
+                                   w, mp, st);
+        if (rc) return rc;
+        if (frames && key.n > 0)
+            INIM_CUDA_TRY(cudaMemcpyAsync(frames + (size_t)(t + 1) * 2 * key.n, dst, pbytes, cudaMemcpyDeviceToDevice, st));
+    }
+    if ((key.iters & 1) && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(pts, pong, pbytes, cudaMemcpyDeviceToDevice, st));
+    return 0;
+}
+
+}  // namespace inim
+
+using namespace inim;
+
+extern "C" {
+
+const char* inim_version(void) { return "libinim sm_100a 0.1"; }
+
+size_t inim_workspace_bytes(int k, int64_t n) {
+    if (!k_ok(k)) return 0;
+    return full_layout(make_geo(k), n).bytes;
+}
+
+int inim_splat(const void* pts, int pts_is_f64, int64_t n, int k, uint32_t* counts, cudaStream_t stream) {
+    if (!k_ok(k) || n < 0 || !counts || (n > 0 && !pts)) return INIM_EINVAL;
+    if (n == 0) return 0;
+    return pts_is_f64 ? launch_splat_f64(static_cast<const double*>(pts), n, k, counts, stream)
+                      : launch_splat_f32(static_cast<const float*>(pts), n, k, counts, nullptr, stream);
+}
+
+int inim_smooth_counts(const uint32_t* counts, int k, int kernel_size, float background, float* d, void* ws,
+                       cudaStream_t stream) {
+    if (!k_ok(k) || !counts || !d || !ws) return INIM_EINVAL;
+    const Geo g = make_geo(k);
+    return launch_smooth_state(counts, true, g, make_ws(ws, make_layout(g)), kernel_size, background, d, true, nullptr,
+                               stream);
+}
+
+int inim_smooth_grid(const float* grid, int k, int kernel_size, float* out, void* ws, cudaStream_t stream) {
+    if (!k_ok(k) || !grid || !out || !ws) return INIM_EINVAL;
+    const Geo g = make_geo(k);
+    return launch_smooth_state(grid, false, g, make_ws(ws, make_layout(g)), kernel_size, 0.f, out, false, nullptr,
+                               stream);
+}
+
+int inim_integral_set(const float* d, int k, float* tables8, double* total, void* ws, cudaStream_t stream) {
+    if (!k_ok(k) || !d || !tables8 || !ws) return INIM_EINVAL;
+    const Geo g = make_geo(k);
+    const Ws w = make_ws(ws, make_layout(g));
+    CUtensorMap map;
+    const CUtensorMap* mp = nullptr;
+    if (g.TW >= 32) {
+        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, g.TH);
+        if (rc) return rc;
+        mp = &map;
+    }
+    int rc = launch_reduce_from_global(d, g, w, mp, stream);
+    if (rc) return rc;
+    rc = launch_carry_scan_state(g, w, nullptr, stream);
+    if (rc) return rc;
+    rc = launch_write_tables(d, g, w, mp, tables8, stream);
+    if (rc) return rc;
+    if (total) INIM_CUDA_TRY(cudaMemcpyAsync(total, w.total, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    return 0;
+}
+
+int inim_column_integrals(const float* d, int k, float* upper, float* lower, cudaStream_t stream) {
+    if (!k_ok(k) || !d || !upper || !lower) return INIM_EINVAL;
+    const int s = 1 << k;
+    int rc = launch_line_scan(d, upper, s, 1, 0, 0, stream);   // rows <= j (integral.py:185)
+    if (rc) return rc;
+    return launch_line_scan(d, lower, s, -1, 0, 1, stream);    // rows > j (integral.py:186)
+}
+
+int inim_line_scan(const float* in, float* out, int k, int dj, int di, int exclusive, cudaStream_t stream) {
+    if (!k_ok(k) || !in || !out || dj < -1 || dj > 1 || di < -1 || di > 1 || (dj == 0 && di == 0)) return INIM_EINVAL;
+    return launch_line_scan(in, out, 1 << k, dj, di, exclusive, stream);
+}
+
+int inim_field_from_density(const float* d, int k, const float* defect, float* targets, float* max_excursion,
+                            double* total, void* ws, cudaStream_t stream) {
+    if (!k_ok(k) || !d || !targets || !max_excursion || !ws) return INIM_EINVAL;
+    const Geo g = make_geo(k);
+    const Ws w = make_ws(ws, make_layout(g));
+    CUtensorMap map;
+    const CUtensorMap* mp = nullptr;
+    if (g.TW >= 32) {
+        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, g.TH);
+        if (rc) return rc;
+        mp = &map;
+    }
+    int rc = launch_reduce_from_global(d, g, w, mp, stream);
+    if (rc) return rc;
+    rc = launch_carry_scan_state(g, w, nullptr, stream);
+    if (rc) return rc;
+    rc = launch_write_field(d, g, w, mp, defect, targets, max_excursion, nullptr, stream);
+    if (rc) return rc;
+    if (total) INIM_CUDA_TRY(cudaMemcpyAsync(total, w.total, sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    return 0;
+}
+
+int inim_field_from_tables(const float* tables8, int k, const double* total, const float* defect, float* targets,
+                           float* max_excursion, cudaStream_t stream) {
+    if (!k_ok(k) || !tables8 || !total || !targets || !max_excursion) return INIM_EINVAL;
+    return launch_field_from_tables(tables8, k, total, defect, targets, max_excursion, stream);
+}
+
+int inim_flat_response(int k, float* defect, cudaStream_t stream) {
+    if (!k_ok(k) || !defect) return INIM_EINVAL;
+    return launch_flat_response(k, defect, stream);
+}
+
+int inim_sample(const float* targets, int k, const float* pts_in, float* pts_out, int64_t n, int clip,
+                float* max_disp, cudaStream_t stream) {
+    if (k < 1 || k > INIM_MAX_K || !targets || n < 0 || (n > 0 && (!pts_in || !pts_out))) return INIM_EINVAL;
+    if (n == 0) return 0;
+    return launch_sample_f32(targets, k, pts_in, pts_out, n, clip, max_disp, nullptr, stream);
+}
+
+int inim_sample_f64(const float* targets, int k, const double* pts_in, double* pts_out, int64_t n, int clip,
+                    cudaStream_t stream) {
+    if (k < 1 || k > INIM_MAX_K || !targets || n < 0 || (n > 0 && (!pts_in || !pts_out))) return INIM_EINVAL;
+    if (n == 0) return 0;
+    return launch_sample_f64(targets, k, pts_in, pts_out, n, clip, stream);
+}
+
+int inim_cast_f64_to_f32(const double* in, float* out, int64_t count, cudaStream_t stream) {
+    if (count < 0 || (count > 0 && (!in || !out))) return INIM_EINVAL;
+    if (count == 0) return 0;
+    return launch_cast_f64_f32(in, out, count, stream);
+}
+
+int inim_cast_f32_to_f64(const float* in, double* out, int64_t count, cudaStream_t stream) {
+    if (count < 0 || (count > 0 && (!in || !out))) return INIM_EINVAL;
+    if (count == 0) return 0;
+    return launch_cast_f32_f64(in, out, count, stream);
+}
+
+int inim_iterate(const float* pts_in, float* pts_out, int64_t n, int k, int kernel_size, float background,
+                 const float* defect, uint32_t* counts, float* d, float* targets, float* max_excursion,
+                 float* disp_out, float stop_eps, int* state, void* ws, cudaStream_t stream) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || !counts || !d || !targets || !max_excursion || !ws) return INIM_EINVAL;
+    if (n > 0 && (!pts_in || !pts_out)) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    if (stop_eps > 0.f && !state) return INIM_EINVAL;
+    const Geo g = make_geo(k);
+    const FullLayout F = full_layout(g, n);
+    const Ws w = make_ws(ws, F.L);
+    float* scratch = reinterpret_cast<float*>(static_cast<char*>(ws) + F.scratch);
+    CUtensorMap map;
+    const CUtensorMap* mp = nullptr;
+    if (g.TW >= 32) {
+        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, g.TH);
+        if (rc) return rc;
+        mp = &map;
+    }
+    return enqueue_iteration(pts_in, pts_out, n, g, kernel_size, auto_background(n, k, background), defect, counts, d,
+                             targets, max_excursion, disp_out ? disp_out : scratch, stop_eps, state, w, mp, stream);
+}
+
+int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
+             float* frames, float* fields, float* disp, float* excursions, int* state, void* ws, cudaStream_t stream) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    if (stop_eps > 0.f && !state) return INIM_EINVAL;
+    if (iterations == 0) return 0;
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations; key.eps = stop_eps; key.frames = frames; key.fields = fields; key.disp = disp;
+    key.exc = excursions; key.state = state; key.ws = ws; key.st = stream;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        for (auto& e : g_cache)
+            if (e.key == key) return (int)cudaGraphLaunch(e.exec, stream);
+    }
+    // First call with these arguments: capture once, keep the executable graph.
+    cudaGraph_t graph;
+    INIM_CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
+    int rc = enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
+    cudaError_t ec = cudaStreamEndCapture(stream, &graph);
+    if (rc) {
+        if (ec == cudaSuccess) cudaGraphDestroy(graph);
+        return rc;
+    }
+    INIM_CUDA_TRY(ec);
+    cudaGraphExec_t exec;
+    ec = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    INIM_CUDA_TRY(ec);
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        if (g_cache.size() >= 16) {
+            cudaGraphExecDestroy(g_cache.front().exec);
+            g_cache.erase(g_cache.begin());
+        }
+        g_cache.push_back({key, exec});
+    }
+    return (int)cudaGraphLaunch(exec, stream);
+}
+
+int inim_run_uncached(float* pts, int64_t n, int k, int kernel_size, float background, int iterations,
+                      float stop_eps, float* frames, float* fields, float* disp, float* excursions, int* state,
+                      void* ws, cudaStream_t stream) {
+    // Same work as inim_run launched eagerly (no graph): used for per-kernel timing.
+    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations; key.eps = stop_eps;
+    return enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
+}
+
+int inim_profile_run(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, void* ws,
+                     cudaStream_t stream, float* ms_out, int cap, char* names_out, int names_len) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 1 || !ws || !ms_out || cap < 1 || (n > 0 && !pts))
+        return INIM_EINVAL;
+    std::vector<cudaEvent_t> ev(cap + 1);
+    std::vector<const char*> names(cap + 1, "");
+    for (auto& e : ev) INIM_CUDA_TRY(cudaEventCreate(&e));
+    Prof p{ev.data(), names.data(), 0, cap + 1};
+    INIM_CUDA_TRY(cudaEventRecord(ev[0], stream));
+    p.names[0] = "start";
+    p.n = 1;
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations;
+    g_prof = &p;
+    int rc = enqueue_run(key, pts, nullptr, nullptr, nullptr, nullptr, nullptr, ws, stream);
+    g_prof = nullptr;
+    if (rc) return rc;
+    INIM_CUDA_TRY(cudaStreamSynchronize(stream));
+    int count = p.n - 1;
+    std::string joined;
+    for (int q = 0; q < count; ++q) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[q], ev[q + 1]);
+        ms_out[q] = ms;
+        joined += names[q + 1];
+        joined += "\n";
+    }
+    if (names_out && names_len > 0) {
+        strncpy(names_out, joined.c_str(), names_len - 1);
+        names_out[names_len - 1] = 0;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return count;
+}
+
+void inim_clear_graph_cache(void) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    for (auto& e : g_cache) cudaGraphExecDestroy(e.exec);
+    g_cache.clear();
+}
+
+int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, int kernel_size, double background,
+                  int iterations) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || (n > 0 && (!pts_host || !out_host))) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    // Grow-only device buffers owned by this entry point (the documented exception to
+    // "the library never allocates").
+    static std::mutex mu;
+    static void* ws = nullptr;
+    static size_t ws_bytes = 0;
+    static double* pd = nullptr;
+    static float* pf = nullptr;
+    static int64_t cap = 0;
+    static cudaStream_t st = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!st) INIM_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const size_t need = inim_workspace_bytes(k, n);
+    if (need > ws_bytes) {
+        if (ws) cudaFree(ws);
+        INIM_CUDA_TRY(cudaMalloc(&ws, need));
+        ws_bytes = need;
+        inim_clear_graph_cache();
+    }
+    if (n > cap) {
+        if (pd) cudaFree(pd);
+        if (pf) cudaFree(pf);
+        INIM_CUDA_TRY(cudaMalloc(&pd, sizeof(double) * 2 * n));
+        INIM_CUDA_TRY(cudaMalloc(&pf, sizeof(float) * 2 * n));
+        cap = n;
+        inim_clear_graph_cache();
+    }
+    if (n > 0) {
+        INIM_CUDA_TRY(cudaMemcpyAsync(pd, pts_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
+        int rc = launch_cast_f64_f32(pd, pf, 2 * n, st);
+        if (rc) return rc;
+    }
+    int rc = inim_run(pf, n, k, kernel_size, (float)background, iterations, 0.f, nullptr, nullptr, nullptr, nullptr,
+                      nullptr, ws, st);
+    if (rc) return rc;
+    if (n > 0) {
+        rc = launch_cast_f32_f64(pf, pd, 2 * n, st);
+        if (rc) return rc;
+        INIM_CUDA_TRY(cudaMemcpyAsync(out_host, pd, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
+    }
+    INIM_CUDA_TRY(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int inim_kernels_per_iteration(int k) {
+    // iter_begin, splat, smooth_h, smooth_v(+reduce), 5 carry-scan kernels, write_field,
+    // sample (+ iter_end when the displacement criterion is on); the memset of the
+    // counts is a graph memset node, not a kernel.
+    (void)k;
+    return 11;
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+// Point-stream kernels: the density splat (reference density.py:14-27 with pixel_of,
+// model.py:189-198) and the bilinear move (mapping.py:207-246 + the clip of
+// regularize.py:36).  Both stream the (n, 2) interleaved positions with 16-byte
+// vector accesses (two points per float4) and touch the grid through L2.
+#include "inim_internal.cuh"
+
+namespace inim {
+
+template <typename T>
+__device__ __forceinline__ int pixel_of(T v, int s) {
+    // i = min(floor(v * s), s - 1); v * s is exact for s = 2^k, so float32 and
+    // float64 coordinates bin identically when the values are identical.
+    const T f = floor(v * (T)s);
+    int i = (int)f;
+    i = i > s - 1 ? s - 1 : i;
+    return i < 0 ? 0 : i;
+}
+
+// Warp-aggregated integer atomics: lanes hitting the same pixel in one step are
+// merged (__match_any_sync) and the leader issues one red.add for the group.
+__device__ __forceinline__ void splat_one(uint32_t* counts, int pix) {
+    const unsigned mask = __match_any_sync(kFull, pix);
+    const int lane = threadIdx.x & 31;
+    if (pix >= 0 && lane == __ffs(mask) - 1) atomicAdd(counts + pix, (uint32_t)__popc(mask));
+}
+
+__global__ void __launch_bounds__(256) splat_f32_kernel(const float4* __restrict__ pts2, const float* __restrict__ pts,
+                                                        int64_t n, int k, uint32_t* __restrict__ counts,
+                                                        const int* state) {
+    if (state && state[0]) return;
+    const int s = 1 << k;
+    const int64_t npair = n >> 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t iters = (npair + stride - 1) / stride;
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t it = 0; it < iters; ++it, p += stride) {
+        int pa = -1, pb = -1;
+        if (p < npair) {
+            const float4 v = __ldcs(pts2 + p);  // streamed: read once per splat
+            pa = pixel_of(v.y, s) * s + pixel_of(v.x, s);
+            pb = pixel_of(v.w, s) * s + pixel_of(v.z, s);
+        }
+        splat_one(counts, pa);
+        splat_one(counts, pb);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const float x = pts[2 * (n - 1)], y = pts[2 * (n - 1) + 1];
+        atomicAdd(counts + pixel_of(y, s) * s + pixel_of(x, s), 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) splat_f64_kernel(const double* __restrict__ pts, int64_t n, int k,
+                                                        uint32_t* __restrict__ counts) {
+    const int s = 1 << k;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t iters = (n + stride - 1) / stride;
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t it = 0; it < iters; ++it, p += stride) {
+        int pix = -1;
+        if (p < n) {
+            const double2 v = reinterpret_cast<const double2*>(pts)[p];
+            pix = pixel_of(v.y, s) * s + pixel_of(v.x, s);
+        }
+        splat_one(counts, pix);
+    }
+}
+
+// _bilinear_kernel (mapping.py:207-232): i0 = clamp(floor(x*s), 0, s-2), fx = x*s - i0
+// (in [1, 2] on the last strip: one-sided extrapolation keeps an identity field the
+// identity), then the four-tap blend, then the clip of regularize.py:36.
+template <typename T>
+__device__ __forceinline__ void bilinear(const float2* __restrict__ tg, int s, T x, T y, T& ox, T& oy) {
+    const T sx = x * (T)s, sy = y * (T)s;
+    int i0 = (int)floor(sx), j0 = (int)floor(sy);
+    i0 = i0 < 0 ? 0 : (i0 > s - 2 ? s - 2 : i0);
+    j0 = j0 < 0 ? 0 : (j0 > s - 2 ? s - 2 : j0);
+    const T fx = sx - (T)i0, fy = sy - (T)j0;
+    const T w00 = ((T)1 - fx) * ((T)1 - fy);
+    const T w10 = fx * ((T)1 - fy);
+    const T w01 = ((T)1 - fx) * fy;
+    const T w11 = fx * fy;
+    const int64_t base = (int64_t)j0 * s + i0;
+    const float2 t00 = __ldg(tg + base), t10 = __ldg(tg + base + 1);
+    const float2 t01 = __ldg(tg + base + s), t11 = __ldg(tg + base + s + 1);
+    ox = w00 * (T)t00.x + w10 * (T)t10.x + w01 * (T)t01.x + w11 * (T)t11.x;
+    oy = w00 * (T)t00.y + w10 * (T)t10.y + w01 * (T)t01.y + w11 * (T)t11.y;
+}
+
+template <typename T>
+__device__ __forceinline__ T clip01(T v) {
+    return v < (T)0 ? (T)0 : (v > (T)1 ? (T)1 : v);
+}
+
+__global__ void __launch_bounds__(256) sample_f32_kernel(const float2* __restrict__ tg, int k,
+                                                         const float4* __restrict__ in2, const float* __restrict__ in,
+                                                         float4* __restrict__ out2, float* __restrict__ out, int64_t n,
+                                                         int clip, float* max_disp, const int* state) {
+    const bool stopped = state && state[0];
+    const int s = 1 << k;
+    const int64_t npair = n >> 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float md = 0.f;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
+        const float4 v = __ldcs(in2 + p);
+        float4 o;
+        if (stopped) {
+            o = v;  // keep the ping-pong buffers consistent after a displacement stop
+        } else {
+            bilinear<float>(tg, s, v.x, v.y, o.x, o.y);
+            bilinear<float>(tg, s, v.z, v.w, o.z, o.w);
+            if (clip) {
+                o.x = clip01(o.x); o.y = clip01(o.y); o.z = clip01(o.z); o.w = clip01(o.w);
+            }
+            md = fmaxf(md, fmaxf(fmaxf(fabsf(o.x - v.x), fabsf(o.y - v.y)), fmaxf(fabsf(o.z - v.z), fabsf(o.w - v.w))));
+        }
+        __stcs(out2 + p, o);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const float x = in[2 * (n - 1)], y = in[2 * (n - 1) + 1];
+        float ox = x, oy = y;
+        if (!stopped) {
+            bilinear<float>(tg, s, x, y, ox, oy);
+            if (clip) { ox = clip01(ox); oy = clip01(oy); }
+            md = fmaxf(md, fmaxf(fabsf(ox - x), fabsf(oy - y)));
+        }
+        out[2 * (n - 1)] = ox;
+        out[2 * (n - 1) + 1] = oy;
+    }
+    if (max_disp && !stopped) {
+        md = warp_max(md);
+        if ((threadIdx.x & 31) == 0 && md > 0.f) atomic_max_nonneg(max_disp, md);
+    }
+}
+
+__global__ void __launch_bounds__(256) sample_f64_kernel(const float2* __restrict__ tg, int k,
+                                                         const double* __restrict__ in, double* __restrict__ out,
+                                                         int64_t n, int clip) {
+    const int s = 1 << k;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += stride) {
+        const double2 v = reinterpret_cast<const double2*>(in)[p];
+        double ox, oy;
+        bilinear<double>(tg, s, v.x, v.y, ox, oy);
+        if (clip) { ox = clip01(ox); oy = clip01(oy); }
+        reinterpret_cast<double2*>(out)[p] = make_double2(ox, oy);
+    }
+}
+
+__global__ void cast_f64_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t count) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = (float)in[q];
+}
+
+__global__ void cast_f32_f64_kernel(const float* __restrict__ in, double* __restrict__ out, int64_t count) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x)
+        out[q] = (double)in[q];
+}
+
+// --------------------------------------------------------------------------- launchers
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+static unsigned grid_for(int64_t work, int per_block) {
+    int64_t blocks = (work + per_block - 1) / per_block;
+    const int64_t cap = (int64_t)sm_count() * 8;  // 8 resident 256-thread CTAs per SM
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
+int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st) {
+    const int64_t npair = n >> 1;
+    splat_f32_kernel<<<grid_for(npair > 0 ? npair : 1, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(pts), pts, n,
+                                                                          k, counts, state);
+    prof_mark(st, "splat");
+    return (int)cudaGetLastError();
+}
+
+int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cudaStream_t st) {
+    splat_f64_kernel<<<grid_for(n > 0 ? n : 1, 256), 256, 0, st>>>(pts, n, k, counts);
+    return (int)cudaGetLastError();
+}
+
+int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
+                      const int* state, cudaStream_t st) {
+    const int64_t npair = n >> 1;
+    sample_f32_kernel<<<grid_for(npair > 0 ? npair : 1, 256), 256, 0, st>>>(
+        reinterpret_cast<const float2*>(tg), k, reinterpret_cast<const float4*>(in), in,
+        reinterpret_cast<float4*>(out), out, n, clip, max_disp, state);
+    prof_mark(st, "sample");
+    return (int)cudaGetLastError();
+}
+
+int launch_sample_f64(const float* tg, int k, const double* in, double* out, int64_t n, int clip, cudaStream_t st) {
+    sample_f64_kernel<<<grid_for(n > 0 ? n : 1, 256), 256, 0, st>>>(reinterpret_cast<const float2*>(tg), k, in, out,
+                                                                     n, clip);
+    return (int)cudaGetLastError();
+}
+
+int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_t st) {
+    cast_f64_f32_kernel<<<grid_for(count > 0 ? count : 1, 256), 256, 0, st>>>(in, out, count);
+    return (int)cudaGetLastError();
+}
+
+int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st) {
+    cast_f32_f64_kernel<<<grid_for(count > 0 ? count : 1, 256), 256, 0, st>>>(in, out, count);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace inim

@@ -1,0 +1,241 @@
+"""Iterative density equalization on the GPU (drop-in for uncrowd regularize.py:25-109).
+
+``run`` keeps every iteration on the device: the positions are narrowed to float32
+once, then chunks of iterations are replayed as one CUDA graph each (inim_run:
+counts <- 0, splat, smoothing + tile reduce, carry scan, fused integral/field,
+bilinear move + clip).  The host only records the frames the reference's frame_cap
+policy keeps and reads the displacement-stop state between chunks.
+"""
+
+from __future__ import annotations
+
+import time
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import _lib
+from .density import build_density, resolve_background
+from .errors import OutOfRangeLevel
+from .mapping import _defect_device, flat_response, sample_points
+from .model import DeformationField, RegularizationParams, RegularizationRun, ScatterDataset
+
+CHUNK = 16  # iterations per captured graph
+
+
+def iterate_once(positions: np.ndarray, params: RegularizationParams, defect: Optional[np.ndarray] = None):
+    """One equalization step: (new positions, field, density) (regularize.py:25-37).
+
+    Float64 positions are binned in float64 (bit-exact counts for identical inputs)
+    and moved with float64 bilinear weights; density and field are float32 on the
+    device.  Sample order is preserved.
+    """
+    lib = D.require_cuda()
+    density = build_density(positions, params)
+    if defect is None:
+        defect = flat_response.get(params.k)
+    k = params.k
+    s = 1 << k
+    dev_def = _defect_device(k, defect, torch.float32)
+    targets = torch.empty((s, s, 2), dtype=torch.float32, device=D.device())
+    exc = torch.zeros(1, dtype=torch.float32, device=D.device())
+    total = torch.empty(1, dtype=torch.float64, device=D.device())
+    ws = D.workspace(k)
+    _lib.check(lib.inim_field_from_density(D.ptr(density.device_values()), k, D.ptr(dev_def), D.ptr(targets),
+                                           D.ptr(exc), D.ptr(total), D.ptr(ws), D.stream()), "iterate_once")
+    field = DeformationField(k=k, max_excursion=float(exc.item()), device_targets=targets)
+    new_positions = sample_points(field, positions, clip=True)
+    return new_positions, field, density
+
+
+def _device_iterate(pos: torch.Tensor, params: RegularizationParams) -> torch.Tensor:
+    """One float32 device iteration (the run loop's own step), used to recompute
+    frames thinned away by frame_cap.  Same kernels as inim_run: bit-identical."""
+    lib = D.require_cuda()
+    n = pos.shape[0]
+    k = params.k
+    s = 1 << k
+    bufs = _run_buffers(n, k, 1, False)
+    out = torch.empty_like(pos)
+    bg = resolve_background(params, n)
+    _lib.check(lib.inim_iterate(D.ptr(pos), D.ptr(out), n, k, params.kernel_size, bg, None, D.ptr(bufs["counts"]),
+                                D.ptr(bufs["d"]), D.ptr(bufs["targets"]), D.ptr(bufs["exc"]), D.ptr(bufs["disp"]),
+                                0.0, None, D.ptr(bufs["ws"]), D.stream()), "iterate")
+    del s
+    return out
+
+
+_bufcache: dict = {}
+
+
+def _run_buffers(n: int, k: int, chunk: int, store_fields: bool):
+    """Persistent device buffers per (n, k, chunk, store_fields): graph replays need
+    stable pointers."""
+    key = (torch.cuda.current_device(), n, k, chunk, store_fields)
+    b = _bufcache.get(key)
+    if b is None:
+        lib = D.require_cuda()
+        s = 1 << k
+        dev = D.device()
+        b = {
+            "ws": torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev),
+            "pts": torch.empty((max(n, 1), 2), dtype=torch.float32, device=dev),
+            "frames": torch.empty((chunk + 1, max(n, 1), 2), dtype=torch.float32, device=dev),
+            "fields": torch.empty((chunk, s, s, 2), dtype=torch.float32, device=dev) if store_fields else None,
+            "disp": torch.zeros(chunk, dtype=torch.float32, device=dev),
+            "excs": torch.zeros(chunk, dtype=torch.float32, device=dev),
+            "state": torch.zeros(4, dtype=torch.int32, device=dev),
+            "counts": torch.empty((s, s), dtype=torch.int32, device=dev),
+            "d": torch.empty((s, s), dtype=torch.float32, device=dev),
+            "targets": torch.empty((s, s, 2), dtype=torch.float32, device=dev),
+            "exc": torch.zeros(1, dtype=torch.float32, device=dev),
+        }
+        if len(_bufcache) > 8:
+            torch.cuda.synchronize()
+            lib.inim_clear_graph_cache()
+            _bufcache.clear()
+        _bufcache[key] = b
+    return b
+
+
+def _survivors(iterations: int, frame_cap: int) -> set:
+    """Frames the reference's thinning policy (model.py:155-162) keeps after a fixed
+    number of iterations."""
+    kept, stride = {0}, 1
+    for t in range(1, iterations + 1):
+        kept.add(t)
+        if len(kept) > frame_cap:
+            stride *= 2
+            kept = {i for i in kept if i in (0, t) or i % stride == 0}
+    return kept
+
+
+def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: str = "none",
+        store_fields: bool = True, n_neighbors: int = 10) -> RegularizationRun:
+    """Repeat iterations until the stopping criterion fires (regularize.py:40-80)."""
+    params.validate()
+    if collect_metrics != "none":
+        raise NotImplementedError("collect_metrics='basic'/'full' needs the metrics subsystem, which is outside "
+                                  "this build's scope (SURVEY.md section 8(f)); use collect_metrics='none'")
+    lib = D.require_cuda()
+    result = RegularizationRun(dataset, params, store_fields=store_fields)
+    flat_response.get(params.k)  # built once per run, as the reference (regularize.py:51)
+    n = dataset.n
+    k = params.k
+    bg = resolve_background(params, n)
+    if params.iterations == 0:
+        return result
+    if params.stop == "time":
+        return _run_timed(result, dataset, params, bg)
+
+    chunk = min(CHUNK, params.iterations)
+    b = _run_buffers(n, k, chunk, store_fields)
+    pts = b["pts"][:n] if n else b["pts"]
+    if n:
+        pts.copy_(D.to_device(dataset.positions).reshape(n, 2))
+    state = b["state"]
+    state.zero_()
+    eps = float(params.epsilon) if params.stop == "displacement" else 0.0
+    keep = _survivors(params.iterations, params.frame_cap) if params.stop == "fixed" else None
+    done = 0
+    stream = D.stream()
+    start_ev = torch.cuda.Event(enable_timing=True)
+    end_ev = torch.cuda.Event(enable_timing=True)
+    while done < params.iterations:
+        c = min(chunk, params.iterations - done)
+        start_ev.record()
+        _lib.check(lib.inim_run(D.ptr(pts), n, k, params.kernel_size, bg, c, eps, D.ptr(b["frames"]),
+                                D.ptr(b["fields"]), D.ptr(b["disp"]), D.ptr(b["excs"]), D.ptr(state),
+                                D.ptr(b["ws"]), stream), "run")
+        end_ev.record()
+        end_ev.synchronize()
+        per_iter = start_ev.elapsed_time(end_ev) / 1e3 / c
+        if eps > 0:
+            st = state.cpu().numpy()
+            executed = int(st[1]) - done
+            stopped = bool(st[0])
+        else:
+            executed, stopped = c, False
+        excs = b["excs"][:executed].cpu().numpy() if executed else []
+        for t in range(executed):
+            it = done + t + 1
+            result.wall_times.append(per_iter)
+            if store_fields:
+                result.fields.append(DeformationField(k=k, max_excursion=float(excs[t]),
+                                                      device_targets=b["fields"][t].clone()))
+            if keep is None or it in keep:
+                result._record(it, b["frames"][t + 1, :n].clone())
+            else:
+                result.iterations = it
+        done += executed
+        if stopped:
+            break
+    return result
+
+
+def _run_timed(result: RegularizationRun, dataset: ScatterDataset, params: RegularizationParams, bg: float):
+    """stop='time': the budget is host wall time, checked between iterations
+    (regularize.py:62-63), so iterations are launched one at a time."""
+    n = dataset.n
+    pos = D.to_device(dataset.positions).reshape(n, 2) if n else torch.zeros((1, 2), device=D.device())
+    started = time.perf_counter()
+    for t in range(1, params.iterations + 1):
+        if time.perf_counter() - started > params.time_budget:
+            break
+        tick = time.perf_counter()
+        new = _device_iterate(pos, params) if n else pos
+        torch.cuda.synchronize()
+        result.wall_times.append(time.perf_counter() - tick)
+        result._record(t, new)
+        pos = new
+    return result
+
+
+def transition_positions(run_result: RegularizationRun, level: float) -> np.ndarray:
+    """Per-sample linear blend between the two frames bracketing `level`
+    (regularize.py:83-93)."""
+    top = run_result.iterations
+    if not 0.0 <= level <= top:
+        raise OutOfRangeLevel(f"level {level} outside [0, {top}]")
+    low, high = int(np.floor(level)), int(np.ceil(level))
+    if low == high:
+        return run_result.frame(low)
+    frac = level - low
+    return (1.0 - frac) * run_result.frame(low) + frac * run_result.frame(high)
+
+
+def map_through(fields, points: np.ndarray, upto: Optional[int] = None) -> np.ndarray:
+    """Push points through the composed per-iteration fields (regularize.py:96-109).
+
+    Fields produced by ``run`` are float32 device fields; points then follow exactly
+    the run's float32 arithmetic, so a sample pushed through ``run.fields`` lands on
+    its frame bit-for-bit.  Fields built in float64 by the caller are applied in
+    float64.
+    """
+    if isinstance(fields, RegularizationRun):
+        fields = fields.fields
+    if upto is None:
+        upto = len(fields)
+    chosen = list(fields[:upto])
+    out = np.asarray(points, dtype=np.float64)
+    if not chosen:
+        return out
+    if any(f.device_targets64() is not None for f in chosen):
+        for f in chosen:
+            out = sample_points(f, out, clip=True)
+        return out
+    lib = D.require_cuda()
+    shape = out.shape
+    flat = out.reshape(-1, 2)
+    n = len(flat)
+    if n == 0:
+        return out
+    a = D.to_device(flat)
+    bbuf = torch.empty_like(a)
+    for f in chosen:
+        _lib.check(lib.inim_sample(D.ptr(f.device_targets()), f.k, D.ptr(a), D.ptr(bbuf), n, 1, None, D.stream()),
+                   "map_through")
+        a, bbuf = bbuf, a
+    return D.to_host64(a).reshape(shape)

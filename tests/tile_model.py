@@ -1,0 +1,131 @@
+"""Pure-numpy model of the device integral pipeline's carry algebra (test helper).
+
+It restates, tile by tile, what csrc/integral.cu computes -- the per-tile aggregates
+(reduce), the float64 carry recurrences over bands (scan) and the per-pixel assembly
+of rect_tl / wedge_up plus the six derived tables (write) -- so the decomposition can
+be checked against the oracle on the CPU, independently of the CUDA code.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _chains(V):
+    """In-tile up-left / up-right chains of the column prefix V (clipped at the tile)."""
+    TH, TW = V.shape
+    UL = np.zeros_like(V)
+    UR = np.zeros_like(V)
+    for r in range(TH):
+        prevL = np.zeros(TW) if r == 0 else np.concatenate([[0.0], UL[r - 1, :-1]])
+        prevR = np.zeros(TW) if r == 0 else np.concatenate([UR[r - 1, 1:], [0.0]])
+        UL[r] = V[r] + prevL
+        UR[r] = V[r] + prevR
+    return UL, UR
+
+
+def geometry(s: int):
+    TH = s if s < 32 else 32
+    TW = 256 if s >= 8192 else (s if s < 128 else 128)
+    return TH, TW
+
+
+def model_tables(d: np.ndarray, TH: int | None = None, TW: int | None = None):
+    d = np.asarray(d, dtype=np.float64)
+    s = d.shape[0]
+    gTH, gTW = geometry(s)
+    TH = TH or gTH
+    TW = TW or gTW
+    B, NX = s // TH, s // TW
+    colsum = np.zeros((B, s))
+    rowsum = np.zeros((s, NX))
+    ulbot = np.zeros((B, s))
+    urbot = np.zeros((B, s))
+    ule = np.zeros((B, NX, TH))
+    ure = np.zeros((B, NX, TH))
+    # ---- reduce
+    for b in range(B):
+        a = b * TH
+        for x in range(NX):
+            i0 = x * TW
+            tile = d[a:a + TH, i0:i0 + TW]
+            V = np.cumsum(tile, axis=0)
+            UL, UR = _chains(V)
+            colsum[b, i0:i0 + TW] = V[-1]
+            rowsum[a:a + TH, x] = tile.sum(axis=1)
+            ulbot[b, i0:i0 + TW] = UL[-1]
+            urbot[b, i0:i0 + TW] = UR[-1]
+            ule[b, x] = UL[:, -1]
+            ure[b, x] = UR[:, 0]
+    # ---- scan
+    ulb2 = ulbot.copy()
+    urb2 = urbot.copy()
+    for b in range(B):
+        for c in range(s):
+            x, u = divmod(c, TW)
+            rr = TH - 2 - u
+            if x > 0 and rr >= 0:
+                ulb2[b, c] += ule[b, x - 1, rr]
+            rq = TH - 1 - (TW - u)
+            if x < NX - 1 and rq >= 0:
+                urb2[b, c] += ure[b, x + 1, rq]
+    batl = np.cumsum(colsum, axis=1)
+    tlcar = np.vstack([np.zeros((1, s)), np.cumsum(batl, axis=0)])
+
+    def TL(b, c):
+        return tlcar[b, c] if c >= 0 else 0.0
+
+    ulcar = np.zeros((B, s))
+    urcar = np.zeros((B, s))
+    for b in range(B - 1):
+        for c in range(s):
+            prev = ulcar[b, c - TH] if c - TH >= 0 else 0.0
+            ulcar[b + 1, c] = ulb2[b, c] + TL(b, c) - TL(b, c - TH) + prev
+            prevr = urcar[b, c + TH] if c + TH < s else 0.0
+            urcar[b + 1, c] = urb2[b, c] + TL(b, min(c + TH - 1, s - 1)) - TL(b, c - 1) + prevr
+    x1 = ulcar - tlcar[:B]
+    x2 = np.zeros((B, s + TH))
+    for b in range(B):
+        for c in range(s):
+            x2[b, c] = urcar[b, c] + TL(b, c - 1)
+        x2[b, s:] = tlcar[b, s - 1]
+    hc = np.concatenate([np.zeros((s, 1)), np.cumsum(rowsum, axis=1)[:, :-1]], axis=1)
+    rtot = rowsum.sum(axis=1)
+    rpre = np.cumsum(rtot)
+    cpre = tlcar[B]
+    C = rpre[-1]
+    jj, ii = np.mgrid[0:s, 0:s]
+    dtot = np.bincount((ii - jj + s - 1).ravel(), weights=d.ravel(), minlength=2 * s - 1)
+    atot = np.bincount((ii + jj).ravel(), weights=d.ravel(), minlength=2 * s - 1)
+    apre = np.cumsum(atot)
+    dsuf = np.cumsum(dtot[::-1])[::-1]
+    # ---- write
+    out = np.zeros((8, s, s))
+    for b in range(B):
+        a = b * TH
+        for x in range(NX):
+            i0 = x * TW
+            tile = d[a:a + TH, i0:i0 + TW]
+            V = np.cumsum(tile, axis=0)
+            UL, UR = _chains(V)
+            for r in range(TH):
+                for u in range(TW):
+                    re = r - u - 1
+                    if re >= 0 and x > 0:
+                        UL[r, u] += ule[b, x - 1, re]
+                    rq = r - (TW - u)
+                    if rq >= 0 and x < NX - 1:
+                        UR[r, u] += ure[b, x + 1, rq]
+            T = UL + UR - V
+            local = np.cumsum(V, axis=1)
+            vh = np.cumsum(hc[a:a + TH, x])
+            for r in range(TH):
+                j = a + r
+                h = r + 1
+                for u in range(TW):
+                    i = i0 + u
+                    tl = tlcar[b, i] + vh[r] + local[r, u]
+                    up = T[r, u] + (x1[b, i - h] if i - h >= 0 else 0.0) + x2[b, i + h]
+                    Rp, Cp, Ap, Ds = rpre[j], cpre[i], apre[i + j], dsuf[i - j + s - 1]
+                    out[:, j, i] = (tl, Cp - tl, C - Rp - Cp + tl, Rp - tl, up, Ap - up, C - Ap - Ds + up, Ds - up)
+    return out, C
