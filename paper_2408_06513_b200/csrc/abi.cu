@@ -330,11 +330,15 @@ int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, in
         for (auto& e : g_cache)
             if (e.key == key) return (int)cudaGraphLaunch(e.exec, stream);
     }
-    // First call with these arguments: capture once, keep the executable graph.
+    // First call with these arguments: capture once (on a private stream: the legacy
+    // default stream cannot be captured), keep the executable graph, launch it on the
+    // caller's stream.
+    static cudaStream_t cap = nullptr;
+    if (!cap) INIM_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     cudaGraph_t graph;
-    INIM_CUDA_TRY(cudaStreamBeginCapture(stream, cudaStreamCaptureModeRelaxed));
-    int rc = enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
-    cudaError_t ec = cudaStreamEndCapture(stream, &graph);
+    INIM_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+    int rc = enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, cap);
+    cudaError_t ec = cudaStreamEndCapture(cap, &graph);
     if (rc) {
         if (ec == cudaSuccess) cudaGraphDestroy(graph);
         return rc;
