@@ -1,10 +1,10 @@
 // Tile geometry and workspace layout of the integral-image pipeline.
 //
 // The texture (s x s, s = 2^k) is cut into bands of TH rows; each band into tiles of
-// TW columns.  One CTA owns one tile; lane u of warp w owns column 32*w + u and sweeps
-// the TH rows.  TH <= 32 (so an in-band diagonal chain crosses at most one warp
-// boundary) and TW >= TH (so a chain ending in a tile's last column stays inside that
-// tile).  See DESIGN.md "Integral pass" for the derivation of every carry.
+// TW columns.  One thread group owns one tile; lane u of warp w owns column 32*w + u
+// and sweeps the TH rows.  TH <= 32 (an in-band diagonal chain crosses at most one
+// warp boundary) and TW >= TH (a chain ending in a tile's last column stays inside
+// that tile).  See DESIGN.md "Integral pass" for the derivation of every carry.
 #pragma once
 
 #include "inim_common.cuh"
@@ -16,12 +16,14 @@ struct Geo {
     int64_t m;
 };
 
+// Bands of 16 rows up to 2048^2 (more CTAs for latency-bound small grids), 32 rows
+// above (fewer carry vectors per pixel for bandwidth-bound large grids).
 inline Geo make_geo(int k) {
     Geo g;
     g.k = k;
     g.s = 1 << k;
     g.m = (int64_t)g.s * g.s;
-    g.TH = g.s < 32 ? g.s : 32;
+    g.TH = g.s < 16 ? g.s : (g.s <= 2048 ? 16 : 32);
     g.TW = g.s >= 8192 ? 256 : (g.s < 128 ? g.s : 128);
     g.B = g.s / g.TH;
     g.NX = g.s / g.TW;
@@ -39,20 +41,18 @@ struct WsLayout {
     size_t urbot;    // float [B][s]           in-tile up-right chain of V at the band's last row
     size_t ule;      // float [B][NX][TH]      up-left chain at each tile's last column
     size_t ure;      // float [B][NX][TH]      up-right chain at each tile's first column
-    size_t dpart;    // float [B][NX][TW+TH-1] per-tile diagonal (i-j) partial sums
-    size_t apart;    // float [B][NX][TW+TH-1] per-tile anti-diagonal (i+j) partial sums
     size_t batl;     // double [B][s]          inclusive row prefix of colsum per band
     size_t ulb2;     // double [B][s]          completed up-left bottom chains
     size_t urb2;     // double [B][s]          completed up-right bottom chains
     size_t tlcar;    // double [B+1][s]        rect_tl at the row above each band (row s-1 for b=B)
     size_t x1;       // double [B][s]          ULcar - TLcar
     size_t x2;       // double [B][s+TH]       URcar + TLcar[c-1], extended with TLcar[s-1]
+    size_t ulrow;    // double [s]             up-left chain of U along the last row (UL[s-1][c])
+    size_t urrow;    // double [s]             up-right chain of U along the last row (UR[s-1][c])
     size_t hc;       // double [s][NX]         row prefix of d up to each tile's first column
-    size_t rpre;     // double [s]             prefix of row totals
+    size_t rpre;     // double [s]             row totals, then their prefix
     size_t apre;     // double [2s-1]          prefix of anti-diagonal totals
     size_t dsuf;     // double [2s-1]          suffix of diagonal totals
-    size_t dtot;     // double [2s-1]          diagonal totals (scratch)
-    size_t atot;     // double [2s-1]          anti-diagonal totals (scratch)
     size_t total;    // double [1]
     size_t misc;     // float [16]             scratch scalars
     size_t bytes;
@@ -68,7 +68,7 @@ inline WsLayout make_layout(const Geo& g) {
         o = align256(o + bytes);
         return r;
     };
-    const size_t s = g.s, B = g.B, NX = g.NX, TH = g.TH, TW = g.TW;
+    const size_t s = g.s, B = g.B, NX = g.NX, TH = g.TH;
     L.tmp = take(sizeof(float) * s * s);
     L.colsum = take(sizeof(float) * B * s);
     L.rowsum = take(sizeof(float) * s * NX);
@@ -76,20 +76,18 @@ inline WsLayout make_layout(const Geo& g) {
     L.urbot = take(sizeof(float) * B * s);
     L.ule = take(sizeof(float) * B * NX * TH);
     L.ure = take(sizeof(float) * B * NX * TH);
-    L.dpart = take(sizeof(float) * B * NX * (TW + TH - 1));
-    L.apart = take(sizeof(float) * B * NX * (TW + TH - 1));
     L.batl = take(sizeof(double) * B * s);
     L.ulb2 = take(sizeof(double) * B * s);
     L.urb2 = take(sizeof(double) * B * s);
     L.tlcar = take(sizeof(double) * (B + 1) * s);
     L.x1 = take(sizeof(double) * B * s);
     L.x2 = take(sizeof(double) * B * (s + TH));
+    L.ulrow = take(sizeof(double) * s);
+    L.urrow = take(sizeof(double) * s);
     L.hc = take(sizeof(double) * s * NX);
     L.rpre = take(sizeof(double) * s);
     L.apre = take(sizeof(double) * (2 * s - 1));
     L.dsuf = take(sizeof(double) * (2 * s - 1));
-    L.dtot = take(sizeof(double) * (2 * s - 1));
-    L.atot = take(sizeof(double) * (2 * s - 1));
     L.total = take(sizeof(double));
     L.misc = take(sizeof(float) * 16);
     L.bytes = o;
@@ -105,20 +103,18 @@ struct Ws {
     float* urbot;
     float* ule;
     float* ure;
-    float* dpart;
-    float* apart;
     double* batl;
     double* ulb2;
     double* urb2;
     double* tlcar;
     double* x1;
     double* x2;
+    double* ulrow;
+    double* urrow;
     double* hc;
     double* rpre;
     double* apre;
     double* dsuf;
-    double* dtot;
-    double* atot;
     double* total;
     float* misc;
 };
@@ -133,20 +129,18 @@ inline Ws make_ws(void* base, const WsLayout& L) {
     w.urbot = reinterpret_cast<float*>(b + L.urbot);
     w.ule = reinterpret_cast<float*>(b + L.ule);
     w.ure = reinterpret_cast<float*>(b + L.ure);
-    w.dpart = reinterpret_cast<float*>(b + L.dpart);
-    w.apart = reinterpret_cast<float*>(b + L.apart);
     w.batl = reinterpret_cast<double*>(b + L.batl);
     w.ulb2 = reinterpret_cast<double*>(b + L.ulb2);
     w.urb2 = reinterpret_cast<double*>(b + L.urb2);
     w.tlcar = reinterpret_cast<double*>(b + L.tlcar);
     w.x1 = reinterpret_cast<double*>(b + L.x1);
     w.x2 = reinterpret_cast<double*>(b + L.x2);
+    w.ulrow = reinterpret_cast<double*>(b + L.ulrow);
+    w.urrow = reinterpret_cast<double*>(b + L.urrow);
     w.hc = reinterpret_cast<double*>(b + L.hc);
     w.rpre = reinterpret_cast<double*>(b + L.rpre);
     w.apre = reinterpret_cast<double*>(b + L.apre);
     w.dsuf = reinterpret_cast<double*>(b + L.dsuf);
-    w.dtot = reinterpret_cast<double*>(b + L.dtot);
-    w.atot = reinterpret_cast<double*>(b + L.atot);
     w.total = reinterpret_cast<double*>(b + L.total);
     w.misc = reinterpret_cast<float*>(b + L.misc);
     return w;
@@ -170,17 +164,13 @@ inline void prof_mark(cudaStream_t st, const char* name) {
 }
 
 // ---------------------------------------------------------------- host-side launchers
-// (defined in integral.cu / smooth.cu; used by run.cu and abi.cu)
 int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map,
                               cudaStream_t st);
-int launch_carry_scan(const Geo& g, const Ws& ws, cudaStream_t st);
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st);
 int launch_write_tables(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, float* tables8,
                         cudaStream_t st);
 int launch_write_field(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const float* defect,
                        float* targets, float* max_exc, const int* state, cudaStream_t st);
-int launch_smooth(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size, float background,
-                  float* d, bool emit_aggregates, const int* state, cudaStream_t st);
 int make_tensor_map_2d(CUtensorMap* map, const float* base, int s, int box_w, int box_h);
 
 }  // namespace inim

@@ -145,7 +145,7 @@ __device__ inline WriteSmem carve_write(unsigned char* base, const Geo& g) {
 }
 
 __host__ __device__ inline size_t reduce_smem_bytes(const Geo& g) {
-    return ((size_t)g.TH * g.TW + 5 * (size_t)g.NW * g.TH) * 4 + 16 + 16;
+    return ((size_t)g.TH * g.TW + 3 * (size_t)g.NW * g.TH) * 4 + 16 + 16;
 }
 
 // Stage the tile of d into shared memory: TMA when the tile is TMA-shaped, otherwise
@@ -319,11 +319,11 @@ __global__ void __launch_bounds__(256) reduce_kernel(const __grid_constant__ CUt
     float* sd = reinterpret_cast<float*>(smem);
     float* rec = sd + g.TH * g.TW;
     uint64_t* bar = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(rec + 5 * g.NW * g.TH) + 15) & ~uintptr_t(15));
+        (reinterpret_cast<uintptr_t>(rec + 3 * g.NW * g.TH) + 15) & ~uintptr_t(15));
     const int x = blockIdx.x, b = blockIdx.y;
     if (use_tma && threadIdx.x == 0) prefetch_tensormap(&map);
     load_tile(sd, bar, &map, d, g, b, x, use_tma);
-    tile_reduce(sd, rec, g, ws, b, x);
+    tile_reduce(sd, rec, g, ws, b, x, threadIdx.x);
 }
 
 template <int MODE>
@@ -337,195 +337,6 @@ __global__ void __launch_bounds__(256) write_kernel(const __grid_constant__ CUte
     if (use_tma && threadIdx.x == 0) prefetch_tensormap(&map);
     load_tile(S.sd, S.bar, &map, d, g, b, x, use_tma);
     tile_write<MODE>(S, g, ws, b, x, out);
-}
-
-// ---- carry scan (phase 2) -----------------------------------------------------------
-
-// Block-wide exclusive scan of one double per thread (blockDim.x <= 1024).
-__device__ double block_exclusive_scan_d(double v, double* sh, double* total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-    const double inc = warp_inclusive_scan_d(v, lane);
-    if (lane == 31) sh[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        const double t = lane < nw ? sh[lane] : 0.0;
-        const double ti = warp_inclusive_scan_d(t, lane);
-        sh[32 + lane] = ti - t;
-        if (lane == 31) sh[64] = ti;
-    }
-    __syncthreads();
-    const double r = sh[32 + w] + inc - v;
-    if (total) *total = sh[64];
-    __syncthreads();
-    return r;
-}
-
-// In-block scan of src[0..n) (strided by `stride`) into dst (double).  dir = +1:
-// inclusive prefix; dir = -1: inclusive suffix.  Deterministic chunked order.
-template <typename T>
-__device__ void block_scan_array(const T* src, double* dst, int n, int dir, double* sh) {
-    const int nt = blockDim.x;
-    const int chunk = (n + nt - 1) / nt;
-    const int t = threadIdx.x;
-    const int lo = t * chunk, hi = min(n, lo + chunk);
-    double acc = 0.0;
-    for (int q = lo; q < hi; ++q) acc += (double)src[dir > 0 ? q : n - 1 - q];
-    const double off = block_exclusive_scan_d(acc, sh, nullptr);
-    double run = off;
-    for (int q = lo; q < hi; ++q) {
-        const int idx = dir > 0 ? q : n - 1 - q;
-        run += (double)src[idx];
-        dst[idx] = run;
-    }
-}
-
-// K2a: per band, inclusive row prefix of the column sums, and completion of the
-// band-bottom chains with the neighbouring tiles' edge chains.
-__global__ void __launch_bounds__(1024) band_rows_kernel(const Geo g, const Ws ws, const int* state) {
-    if (state && state[0]) return;
-    __shared__ double sh[72];
-    const int b = blockIdx.x, s = g.s, TH = g.TH, TW = g.TW, NX = g.NX;
-    block_scan_array<float>(ws.colsum + (int64_t)b * s, ws.batl + (int64_t)b * s, s, +1, sh);
-    for (int c = threadIdx.x; c < s; c += blockDim.x) {
-        const int x = c / TW, u = c % TW;
-        double ul = ws.ulbot[(int64_t)b * s + c];
-        const int rr = TH - 2 - u;  // row where the chain leaves the tile on the left
-        if (x > 0 && rr >= 0) ul += ws.ule[((int64_t)b * NX + x - 1) * TH + rr];
-        double ur = ws.urbot[(int64_t)b * s + c];
-        const int rq = TH - 1 - (TW - u);
-        if (x < NX - 1 && rq >= 0) ur += ws.ure[((int64_t)b * NX + x + 1) * TH + rq];
-        ws.ulb2[(int64_t)b * s + c] = ul;
-        ws.urb2[(int64_t)b * s + c] = ur;
-    }
-}
-
-// K2b: TLcar_b[c] = sum_{b' < b} BATL[b'][c]  (rect_tl at the row above band b).
-__global__ void band_cols_kernel(const Geo g, const Ws ws, const int* state) {
-    if (state && state[0]) return;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= g.s) return;
-    const int s = g.s;
-    double acc = 0.0;
-    ws.tlcar[c] = 0.0;
-    for (int b = 0; b < g.B; ++b) {
-        acc += ws.batl[(int64_t)b * s + c];
-        ws.tlcar[(int64_t)(b + 1) * s + c] = acc;
-    }
-}
-
-// K2c: the diagonal carries.  Up-left: ULcar_{b+1}[c] = ULbot_b[c] + TLcar_b[c] -
-// TLcar_b[c-TH] + ULcar_b[c-TH]; up-right: URcar_{b+1}[c] = URbot_b[c] +
-// TLcar_b[min(c+TH-1, s-1)] - TLcar_b[c-1] + URcar_b[c+TH].  Each thread walks one
-// chain through the bands.  Outputs X1 = ULcar - TLcar and X2 = URcar + TLcar[c-1].
-__global__ void diag_kernel(const Geo g, const Ws ws, const int* state) {
-    if (state && state[0]) return;
-    const int s = g.s, TH = g.TH, B = g.B;
-    const int nul = s + (B - 1) * TH;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    auto TL = [&](int b, int c) -> double { return c >= 0 ? ws.tlcar[(int64_t)b * s + c] : 0.0; };
-    if (q < nul) {
-        int b, c;
-        double car;
-        if (q < s) {
-            b = 0; c = q; car = 0.0;
-        } else {
-            b = 1 + (q - s) / TH; c = (q - s) % TH;
-            car = ws.ulb2[(int64_t)(b - 1) * s + c] + TL(b - 1, c);
-        }
-        while (true) {
-            ws.x1[(int64_t)b * s + c] = car - TL(b, c);
-            if (b + 1 >= B || c + TH >= s) break;
-            car = ws.ulb2[(int64_t)b * s + c + TH] + TL(b, c + TH) - TL(b, c) + car;
-            b += 1;
-            c += TH;
-        }
-        return;
-    }
-    const int q2 = q - nul;
-    if (q2 < nul) {
-        int b, c;
-        double car;
-        if (q2 < s) {
-            b = 0; c = q2; car = 0.0;
-        } else {
-            b = 1 + (q2 - s) / TH; c = s - TH + (q2 - s) % TH;
-            car = ws.urb2[(int64_t)(b - 1) * s + c] + TL(b - 1, min(c + TH - 1, s - 1)) - TL(b - 1, c - 1);
-        }
-        while (true) {
-            ws.x2[(int64_t)b * (s + TH) + c] = car + TL(b, c - 1);
-            if (b + 1 >= B || c - TH < 0) break;
-            const int cn = c - TH;
-            car = ws.urb2[(int64_t)b * s + cn] + TL(b, min(cn + TH - 1, s - 1)) - TL(b, cn - 1) + car;
-            b += 1;
-            c = cn;
-        }
-        return;
-    }
-    const int q3 = q2 - nul;
-    if (q3 < B * TH) {  // X2 beyond the right border: TLcar_b[s-1]
-        const int b = q3 / TH, e = q3 % TH;
-        ws.x2[(int64_t)b * (s + TH) + s + e] = TL(b, s - 1);
-    }
-}
-
-// K2d1: row totals + row carries HC, and diagonal / anti-diagonal totals.
-__global__ void marg_partial_kernel(const Geo g, const Ws ws, const int* state) {
-    if (state && state[0]) return;
-    const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX, B = g.B;
-    const int ND = TW + TH - 1;
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < s) {
-        double acc = 0.0;
-        for (int x = 0; x < NX; ++x) {
-            ws.hc[(int64_t)q * NX + x] = acc;
-            acc += (double)ws.rowsum[(int64_t)q * NX + x];
-        }
-        ws.rpre[q] = acc;  // row total (scanned by marg_scan_kernel)
-    }
-    if (q < 2 * s - 1) {
-        // diagonal delta = q - (s-1): tile-local t = delta - i0 + a + TH - 1
-        const int delta = q - (s - 1);
-        double dacc = 0.0, aacc = 0.0;
-        const int sigma = q;
-        for (int b = 0; b < B; ++b) {
-            const int a = b * TH;
-            {
-                int lo = delta + a - TW + 1, hi = delta + a + TH - 1;  // i0 range
-                int xlo = lo <= 0 ? 0 : (lo + TW - 1) / TW;
-                int xhi = hi < 0 ? -1 : min(NX - 1, hi / TW);
-                for (int x = xlo; x <= xhi; ++x) {
-                    const int t = delta - x * TW + a + TH - 1;
-                    if (t >= 0 && t < ND) dacc += (double)ws.dpart[((int64_t)b * NX + x) * ND + t];
-                }
-            }
-            {
-                int lo = sigma - a - TW - TH + 2, hi = sigma - a;
-                int xlo = lo <= 0 ? 0 : (lo + TW - 1) / TW;
-                int xhi = hi < 0 ? -1 : min(NX - 1, hi / TW);
-                for (int x = xlo; x <= xhi; ++x) {
-                    const int t = sigma - x * TW - a;
-                    if (t >= 0 && t < ND) aacc += (double)ws.apart[((int64_t)b * NX + x) * ND + t];
-                }
-            }
-        }
-        ws.dtot[q] = dacc;
-        ws.atot[q] = aacc;
-    }
-}
-
-// K2d2: prefix of row totals, prefix of anti-diagonal totals, suffix of diagonal
-// totals, total mass.  One block.
-__global__ void __launch_bounds__(1024) marg_scan_kernel(const Geo g, const Ws ws, const int* state) {
-    if (state && state[0]) return;
-    __shared__ double sh[72];
-    const int s = g.s;
-    block_scan_array<double>(ws.rpre, ws.rpre, s, +1, sh);
-    __syncthreads();
-    block_scan_array<double>(ws.atot, ws.apre, 2 * s - 1, +1, sh);
-    __syncthreads();
-    block_scan_array<double>(ws.dtot, ws.dsuf, 2 * s - 1, -1, sh);
-    __syncthreads();
-    if (threadIdx.x == 0) *ws.total = ws.rpre[s - 1];
 }
 
 // ---- standalone helpers ----------------------------------------------------------------
@@ -625,25 +436,6 @@ int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const 
     return (int)cudaGetLastError();
 }
 
-int launch_carry_scan(const Geo& g, const Ws& ws, cudaStream_t st) {
-    return launch_carry_scan_state(g, ws, nullptr, st);
-}
-
-int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st) {
-    band_rows_kernel<<<g.B, 1024, 0, st>>>(g, ws, state);
-    prof_mark(st, "band_rows");
-    band_cols_kernel<<<(g.s + 255) / 256, 256, 0, st>>>(g, ws, state);
-    prof_mark(st, "band_cols");
-    const int nul = g.s + (g.B - 1) * g.TH;
-    const int nthreads = 2 * nul + g.B * g.TH;
-    diag_kernel<<<(nthreads + 127) / 128, 128, 0, st>>>(g, ws, state);
-    prof_mark(st, "diag_carry");
-    marg_partial_kernel<<<(2 * g.s - 1 + 127) / 128, 128, 0, st>>>(g, ws, state);
-    prof_mark(st, "marg_partial");
-    marg_scan_kernel<<<1, 1024, 0, st>>>(g, ws, state);
-    prof_mark(st, "marg_scan");
-    return (int)cudaGetLastError();
-}
 
 template <int MODE>
 static int launch_write_mode(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map,

@@ -25,7 +25,7 @@ def _chains(V):
 
 
 def geometry(s: int):
-    TH = s if s < 32 else 32
+    TH = s if s < 16 else (16 if s <= 2048 else 32)
     TW = 256 if s >= 8192 else (s if s < 128 else 128)
     return TH, TW
 
@@ -75,15 +75,15 @@ def model_tables(d: np.ndarray, TH: int | None = None, TW: int | None = None):
     def TL(b, c):
         return tlcar[b, c] if c >= 0 else 0.0
 
-    ulcar = np.zeros((B, s))
-    urcar = np.zeros((B, s))
-    for b in range(B - 1):
+    ulcar = np.zeros((B + 1, s))
+    urcar = np.zeros((B + 1, s))
+    for b in range(B):
         for c in range(s):
             prev = ulcar[b, c - TH] if c - TH >= 0 else 0.0
             ulcar[b + 1, c] = ulb2[b, c] + TL(b, c) - TL(b, c - TH) + prev
             prevr = urcar[b, c + TH] if c + TH < s else 0.0
             urcar[b + 1, c] = urb2[b, c] + TL(b, min(c + TH - 1, s - 1)) - TL(b, c - 1) + prevr
-    x1 = ulcar - tlcar[:B]
+    x1 = ulcar[:B] - tlcar[:B]
     x2 = np.zeros((B, s + TH))
     for b in range(B):
         for c in range(s):
@@ -94,11 +94,28 @@ def model_tables(d: np.ndarray, TH: int | None = None, TW: int | None = None):
     rpre = np.cumsum(rtot)
     cpre = tlcar[B]
     C = rpre[-1]
-    jj, ii = np.mgrid[0:s, 0:s]
-    dtot = np.bincount((ii - jj + s - 1).ravel(), weights=d.ravel(), minlength=2 * s - 1)
-    atot = np.bincount((ii + jj).ravel(), weights=d.ravel(), minlength=2 * s - 1)
-    apre = np.cumsum(atot)
-    dsuf = np.cumsum(dtot[::-1])[::-1]
+    # diagonal / anti-diagonal marginals from the chains (no per-tile partial sums):
+    #   Dsuf[delta>=0] = UL[s-1-delta][s-1],  Dsuf[delta<0] = UL[s-1][s-1+delta] + C - Cpre[s-1+delta]
+    #   Apre[sigma<s]  = UR[sigma][0],        Apre[sigma>=s] = UR[s-1][sigma-s+1] + Cpre[sigma-s]
+    dsuf = np.zeros(2 * s - 1)
+    apre = np.zeros(2 * s - 1)
+    for q in range(2 * s - 1):
+        delta = q - (s - 1)
+        if delta >= 0:
+            j = s - 1 - delta
+            b, r = divmod(j, TH)
+            c2 = s - 2 - r
+            dsuf[q] = ule[b, NX - 1, r] + tlcar[b, s - 1] + (x1[b, c2] if c2 >= 0 else 0.0)
+        else:
+            c = s - 1 + delta
+            dsuf[q] = ulcar[B, c] + C - cpre[c]
+        sigma = q
+        if sigma < s:
+            b, r = divmod(sigma, TH)
+            apre[q] = ure[b, 0, r] + x2[b, r + 1]
+        else:
+            i = sigma - (s - 1)
+            apre[q] = urcar[B, i] + cpre[i - 1]
     # ---- write
     out = np.zeros((8, s, s))
     for b in range(B):
