@@ -10,7 +10,8 @@
 #include "inim_internal.cuh"
 
 namespace inim {
-int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st);
+int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st,
+                     float* zero0 = nullptr, float* zero1 = nullptr);
 int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cudaStream_t st);
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
                       const int* state, cudaStream_t st);
@@ -19,38 +20,34 @@ int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_
 int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st);
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st);
 int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
-                        float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st);
+                        float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
+                        uint32_t* zero_next = nullptr);
 int launch_field_from_tables(const float* t8, int k, const double* total, const float* defect, float* targets,
                              float* max_exc, cudaStream_t st);
 int launch_flat_response(int k, float* defect, cudaStream_t st);
 int launch_line_scan(const float* in, float* out, int s, int dj, int di, int exclusive, cudaStream_t st);
+int cell_count(int k);
+int launch_sort_points(const float* pts, int64_t n, int k, int* hist, int* rank, float* sorted, int* perm,
+                       cudaStream_t st);
+int launch_unpermute(const float* sorted, const int* perm, int64_t n, float* out, cudaStream_t st);
 
 // Per-iteration bookkeeping for the displacement criterion (regularize.py:76-79).
-__global__ void iter_begin_kernel(float* max_exc, float* disp, const int* state) {
-    if (state && state[0]) return;
-    if (max_exc) *max_exc = 0.f;
-    if (disp) *disp = 0.f;
-}
-
 __global__ void iter_end_kernel(const float* disp, float eps, int* state) {
     if (state[0]) return;
     state[1] += 1;
     if (*disp < eps) state[0] = 1;
 }
 
-struct IterBufs {
-    uint32_t* counts;
-    float* d;
-    float* targets;
-    float* scratch;  // >= 4 floats
-    float* pong;     // n*2 floats (run only)
-};
-
-// Workspace = integral layout + grid buffers + point ping-pong.
+// Workspace = integral layout + grid buffers (two count buffers: the splat of
+// iteration t+1 fills the one the smoothing of iteration t cleared; the flat response
+// for grids up to 2048^2, read from L2 instead of re-derived per pixel) + point
+// ping-pong.
 struct FullLayout {
     WsLayout L;
-    size_t counts, d, targets, scratch, pong, bytes;
+    size_t counts, d, targets, defect, scratch, sortA, sortB, perm, rank, hist, bytes;
 };
+
+static bool precomputed_defect(const Geo& g) { return g.s <= 2048; }
 
 static FullLayout full_layout(const Geo& g, int64_t n) {
     FullLayout F;
@@ -61,29 +58,33 @@ static FullLayout full_layout(const Geo& g, int64_t n) {
         o = align256(o + bytes);
         return r;
     };
-    F.counts = take(sizeof(uint32_t) * g.m);
+    F.counts = take(sizeof(uint32_t) * 2 * g.m);
     F.d = take(sizeof(float) * g.m);
     F.targets = take(sizeof(float) * 2 * g.m);
+    F.defect = take(precomputed_defect(g) ? sizeof(float) * 2 * g.m : 0);
     F.scratch = take(sizeof(float) * 64);
-    F.pong = take(sizeof(float) * 2 * (size_t)(n > 0 ? n : 1));
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    F.sortA = take(sizeof(float) * 2 * nn);  // points in cell order (ping)
+    F.sortB = take(sizeof(float) * 2 * nn);  // (pong)
+    F.perm = take(sizeof(int) * nn);         // sorted slot -> input row
+    F.rank = take(sizeof(int) * nn);
+    F.hist = take(sizeof(int) * (size_t)cell_count(g.k));
     F.bytes = o;
     return F;
 }
 
 static bool k_ok(int k) { return k >= 0 && k <= INIM_MAX_K; }
 
+// One iteration.  `counts` must be zero on entry; `counts_next` (optional) is cleared
+// by the smoothing pass for the next iteration.
 static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, const Geo& g, int kernel_size,
-                             float background, const float* defect, uint32_t* counts, float* d, float* targets,
-                             float* max_exc, float* disp, float stop_eps, int* state, const Ws& ws,
+                             float background, const float* defect, uint32_t* counts, uint32_t* counts_next, float* d,
+                             float* targets, float* max_exc, float* disp, float stop_eps, int* state, const Ws& ws,
                              const CUtensorMap* map, cudaStream_t st) {
     const int* flag = stop_eps > 0.f ? state : nullptr;
-    iter_begin_kernel<<<1, 1, 0, st>>>(max_exc, disp, flag);
-    prof_mark(st, "iter_begin");
-    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * g.m, st));
-    prof_mark(st, "memset_counts");
-    int rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st);
+    int rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp);
     if (rc) return rc;
-    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st);
+    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, ws, flag, st);
     if (rc) return rc;
@@ -136,8 +137,13 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     uint32_t* counts = reinterpret_cast<uint32_t*>(base + F.counts);
     float* d = reinterpret_cast<float*>(base + F.d);
     float* tg_scratch = reinterpret_cast<float*>(base + F.targets);
+    float* defect = precomputed_defect(g) ? reinterpret_cast<float*>(base + F.defect) : nullptr;
     float* scratch = reinterpret_cast<float*>(base + F.scratch);
-    float* pong = reinterpret_cast<float*>(base + F.pong);
+    float* sortA = reinterpret_cast<float*>(base + F.sortA);
+    float* sortB = reinterpret_cast<float*>(base + F.sortB);
+    int* perm = reinterpret_cast<int*>(base + F.perm);
+    int* rank = reinterpret_cast<int*>(base + F.rank);
+    int* hist = reinterpret_cast<int*>(base + F.hist);
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (g.TW >= 32) {
@@ -145,22 +151,46 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         if (rc) return rc;
         mp = &map;
     }
+    // once per run: both count buffers cleared, the flat response laid out
+    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * 2 * g.m, st));
+    prof_mark(st, "memset_counts");
+    if (defect) {
+        int rc = launch_flat_response(g.k, defect, st);
+        if (rc) return rc;
+    }
     const size_t pbytes = sizeof(float) * 2 * (size_t)key.n;
     if (frames && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(frames, pts, pbytes, cudaMemcpyDeviceToDevice, st));
-    float* bufs[2] = {pts, pong};
+    // Optional spatial pre-sort of the points (kSortPoints): a single counting sort by
+    // cell; off until its hot-cell atomics are privatised (it currently costs more than
+    // the gathers it saves).
+    constexpr bool kSortPoints = false;
+    if (key.n > 0) {
+        int rc = kSortPoints ? launch_sort_points(pts, key.n, g.k, hist, rank, sortA, perm, st)
+                             : (int)cudaMemcpyAsync(sortA, pts, pbytes, cudaMemcpyDeviceToDevice, st);
+        if (rc) return rc;
+    }
+    float* bufs[2] = {sortA, sortB};
     for (int t = 0; t < key.iters; ++t) {
         float* src = bufs[t & 1];
         float* dst = bufs[(t + 1) & 1];
         float* tg = fields ? fields + (size_t)t * 2 * g.m : tg_scratch;
         float* dsp = disp ? disp + t : scratch;
         float* ex = excursions ? excursions + t : scratch + 1;
-        int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, nullptr, counts, d, tg, ex, dsp, key.eps, state,
-                                   w, mp, st);
+        uint32_t* cur = counts + (size_t)(t & 1) * g.m;
+        uint32_t* next = counts + (size_t)((t + 1) & 1) * g.m;
+        int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, tg, ex, dsp, key.eps,
+                                   state, w, mp, st);
         if (rc) return rc;
-        if (frames && key.n > 0)
-            INIM_CUDA_TRY(cudaMemcpyAsync(frames + (size_t)(t + 1) * 2 * key.n, dst, pbytes, cudaMemcpyDeviceToDevice, st));
+        if (frames && key.n > 0) {
+            float* fr = frames + (size_t)(t + 1) * 2 * key.n;
+            rc = kSortPoints ? launch_unpermute(dst, perm, key.n, fr, st)
+                             : (int)cudaMemcpyAsync(fr, dst, pbytes, cudaMemcpyDeviceToDevice, st);
+            if (rc) return rc;
+        }
     }
-    if ((key.iters & 1) && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(pts, pong, pbytes, cudaMemcpyDeviceToDevice, st));
+    if (key.n > 0)
+        return kSortPoints ? launch_unpermute(bufs[key.iters & 1], perm, key.n, pts, st)
+                           : (int)cudaMemcpyAsync(pts, bufs[key.iters & 1], pbytes, cudaMemcpyDeviceToDevice, st);
     return 0;
 }
 
@@ -310,8 +340,10 @@ int inim_iterate(const float* pts_in, float* pts_out, int64_t n, int k, int kern
         if (rc) return rc;
         mp = &map;
     }
-    return enqueue_iteration(pts_in, pts_out, n, g, kernel_size, auto_background(n, k, background), defect, counts, d,
-                             targets, max_excursion, disp_out ? disp_out : scratch, stop_eps, state, w, mp, stream);
+    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * g.m, stream));
+    return enqueue_iteration(pts_in, pts_out, n, g, kernel_size, auto_background(n, k, background), defect, counts,
+                             nullptr, d, targets, max_excursion, disp_out ? disp_out : scratch, stop_eps, state, w, mp,
+                             stream);
 }
 
 int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
@@ -463,11 +495,11 @@ int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, in
 }
 
 int inim_kernels_per_iteration(int k) {
-    // iter_begin, splat, smooth_h, smooth_v(+reduce), 5 carry-scan kernels, write_field,
-    // sample (+ iter_end when the displacement criterion is on); the memset of the
-    // counts is a graph memset node, not a kernel.
+    // splat, smooth_h, smooth_v(+reduce), 4 carry-scan kernels, write_field, sample
+    // (+ iter_end when the displacement criterion is on).  Per run, not per iteration:
+    // one memset node and one flat-response kernel (grids <= 2048^2).
     (void)k;
-    return 11;
+    return 9;
 }
 
 }  // extern "C"

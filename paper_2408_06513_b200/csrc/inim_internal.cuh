@@ -1,10 +1,9 @@
 // Tile geometry and workspace layout of the integral-image pipeline.
 //
 // The texture (s x s, s = 2^k) is cut into bands of TH rows; each band into tiles of
-// TW columns.  One thread group owns one tile; lane u of warp w owns column 32*w + u
-// and sweeps the TH rows.  TH <= 32 (an in-band diagonal chain crosses at most one
-// warp boundary) and TW >= TH (a chain ending in a tile's last column stays inside
-// that tile).  See DESIGN.md "Integral pass" for the derivation of every carry.
+// TW = 32 * CPL columns.  One warp owns one tile; lane l owns columns CPL*l .. CPL*l +
+// CPL - 1 and sweeps the TH rows.  TH <= 32 (lane-distributed row constants) and
+// TW >= TH (a chain ending in a tile's last column stays inside that tile).  See DESIGN.md "Integral pass" for the derivation of every carry.
 #pragma once
 
 #include "inim_common.cuh"
@@ -12,7 +11,7 @@
 namespace inim {
 
 struct Geo {
-    int k, s, TH, TW, B, NX, NW, WL;  // WL = lanes per warp holding columns (32, or TW if TW < 32)
+    int k, s, TH, TW, B, NX, NW, WL, CPL;  // WL = lanes holding columns; CPL = columns per lane
     int64_t m;
 };
 
@@ -24,10 +23,13 @@ inline Geo make_geo(int k) {
     g.s = 1 << k;
     g.m = (int64_t)g.s * g.s;
     g.TH = g.s < 16 ? g.s : (g.s <= 2048 ? 16 : 32);
-    g.TW = g.s >= 8192 ? 256 : (g.s < 128 ? g.s : 128);
+    // one warp per tile: 64 columns (2 per lane) up to 2048^2 for more warps on small
+    // grids, 128 columns (4 per lane, 16-byte accesses) above
+    g.TW = g.s <= 2048 ? (g.s < 64 ? g.s : 64) : 128;
+    g.CPL = g.TW >= 128 ? 4 : (g.TW >= 64 ? 2 : 1);
     g.B = g.s / g.TH;
     g.NX = g.s / g.TW;
-    g.NW = g.TW >= 32 ? g.TW / 32 : 1;
+    g.NW = 1;
     g.WL = g.TW >= 32 ? 32 : g.TW;
     return g;
 }

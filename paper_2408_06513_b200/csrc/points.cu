@@ -24,24 +24,25 @@ __device__ __forceinline__ void splat_one(uint32_t* counts, int pix) {
     if (pix >= 0 && lane == __ffs(mask) - 1) atomicAdd(counts + pix, (uint32_t)__popc(mask));
 }
 
+// The iteration's splat.  Points are in no particular spatial order, so lanes rarely
+// share a pixel: plain red.global.add (no return) per point, two points per 16-byte
+// load.  zero0/zero1: per-iteration device scalars (max excursion, max displacement)
+// cleared here so the iteration needs no separate reset launch.
 __global__ void __launch_bounds__(256) splat_f32_kernel(const float4* __restrict__ pts2, const float* __restrict__ pts,
                                                         int64_t n, int k, uint32_t* __restrict__ counts,
-                                                        const int* state) {
+                                                        const int* state, float* zero0, float* zero1) {
     if (state && state[0]) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (zero0) *zero0 = 0.f;
+        if (zero1) *zero1 = 0.f;
+    }
     const int s = 1 << k;
     const int64_t npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t iters = (npair + stride - 1) / stride;
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t it = 0; it < iters; ++it, p += stride) {
-        int pa = -1, pb = -1;
-        if (p < npair) {
-            const float4 v = __ldcs(pts2 + p);  // streamed: read once per splat
-            pa = pixel_of(v.y, s) * s + pixel_of(v.x, s);
-            pb = pixel_of(v.w, s) * s + pixel_of(v.z, s);
-        }
-        splat_one(counts, pa);
-        splat_one(counts, pb);
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
+        const float4 v = __ldcs(pts2 + p);  // streamed: read once per splat
+        atomicAdd(counts + pixel_of(v.y, s) * s + pixel_of(v.x, s), 1u);
+        atomicAdd(counts + pixel_of(v.w, s) * s + pixel_of(v.z, s), 1u);
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const float x = pts[2 * (n - 1)], y = pts[2 * (n - 1) + 1];
@@ -146,6 +147,80 @@ __global__ void __launch_bounds__(256) sample_f64_kernel(const float2* __restric
     }
 }
 
+// ---------------------------------------------------------------- spatial point order
+// A counting sort of the points by 16 x 16-pixel cell, done once per run: consecutive
+// points (one warp) then fall in the same few cells, so the splat's atomics aggregate
+// and the bilinear gathers hit L1.  No result depends on the order (integer counts,
+// independent per-point moves); frames are scattered back through `perm`.
+constexpr int kCellShift = 4;
+
+__device__ __forceinline__ int cell_of(float x, float y, int k) {
+    const int s = 1 << k;
+    const int cs = k > kCellShift ? k - kCellShift : 0;  // log2(cells per side)
+    const int sh = k - cs;
+    return (pixel_of(y, s) >> sh) * (1 << cs) + (pixel_of(x, s) >> sh);
+}
+
+__global__ void __launch_bounds__(256) cell_count_kernel(const float2* __restrict__ pts, int64_t n, int k,
+                                                         int* __restrict__ hist, int* __restrict__ rank) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = pts[p];
+        rank[p] = atomicAdd(hist + cell_of(v.x, v.y, k), 1);
+    }
+}
+
+// Exclusive scan of the cell histogram, one block (cells <= 65536 for k <= 12,
+// 1M for k = 14: loops over tiles).
+__global__ void __launch_bounds__(1024) cell_scan_kernel(int* __restrict__ hist, int ncells) {
+    __shared__ int sh[33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int carry = 0;
+    for (int base = 0; base < ncells; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int v = i < ncells ? hist[i] : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) sh[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const int t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+            int ti = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(kFull, ti, o);
+                if (lane >= o) ti += u;
+            }
+            sh[lane] = ti - t;
+            if (lane == 31) sh[32] = ti;
+        }
+        __syncthreads();
+        if (i < ncells) hist[i] = carry + sh[w] + inc - v;
+        carry += sh[32];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) cell_scatter_kernel(const float2* __restrict__ pts, int64_t n, int k,
+                                                           const int* __restrict__ offs, const int* __restrict__ rank,
+                                                           float2* __restrict__ sorted, int* __restrict__ perm) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = pts[p];
+        const int dst = offs[cell_of(v.x, v.y, k)] + rank[p];
+        sorted[dst] = v;
+        perm[dst] = (int)p;
+    }
+}
+
+__global__ void __launch_bounds__(256) unpermute_kernel(const float2* __restrict__ sorted, const int* __restrict__ perm,
+                                                        int64_t n, float2* __restrict__ out) {
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+        out[perm[q]] = sorted[q];
+}
+
 __global__ void cast_f64_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t count) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x)
         out[q] = (float)in[q];
@@ -175,11 +250,38 @@ static unsigned grid_for(int64_t work, int per_block) {
     return (unsigned)(blocks < 1 ? 1 : blocks);
 }
 
-int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st) {
+int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st,
+                     float* zero0, float* zero1) {
     const int64_t npair = n >> 1;
     splat_f32_kernel<<<grid_for(npair > 0 ? npair : 1, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(pts), pts, n,
-                                                                          k, counts, state);
+                                                                          k, counts, state, zero0, zero1);
     prof_mark(st, "splat");
+    return (int)cudaGetLastError();
+}
+
+int cell_count(int k) {
+    const int cs = k > kCellShift ? k - kCellShift : 0;
+    return 1 << (2 * cs);
+}
+
+// hist: cell_count(k) ints (zeroed here); rank, perm: n ints; sorted: n float2.
+int launch_sort_points(const float* pts, int64_t n, int k, int* hist, int* rank, float* sorted, int* perm,
+                       cudaStream_t st) {
+    const int nc = cell_count(k);
+    INIM_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * nc, st));
+    const unsigned grid = grid_for(n > 0 ? n : 1, 256);
+    cell_count_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(pts), n, k, hist, rank);
+    cell_scan_kernel<<<1, 1024, 0, st>>>(hist, nc);
+    cell_scatter_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(pts), n, k, hist, rank,
+                                              reinterpret_cast<float2*>(sorted), perm);
+    prof_mark(st, "sort_points");
+    return (int)cudaGetLastError();
+}
+
+int launch_unpermute(const float* sorted, const int* perm, int64_t n, float* out, cudaStream_t st) {
+    unpermute_kernel<<<grid_for(n > 0 ? n : 1, 256), 256, 0, st>>>(reinterpret_cast<const float2*>(sorted), perm, n,
+                                                                    reinterpret_cast<float2*>(out));
+    prof_mark(st, "unpermute");
     return (int)cudaGetLastError();
 }
 

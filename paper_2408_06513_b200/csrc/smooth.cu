@@ -71,9 +71,12 @@ inline size_t h_smem_bytes(const HGeo& h, int R) {
     return ((size_t)(h.TWH + 2 * R) * (h.RH + 1) + (size_t)h.RH * (h.TWH + 1)) * sizeof(float);
 }
 
+// zero_next (optional): the other counts buffer of the iteration's ping-pong pair; each
+// CTA clears its own RH x TWH block of it, so the next splat needs no memset.
 template <int R, typename T>
 __global__ void __launch_bounds__(256) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
-                                                       const HGeo h, const Taps taps, const int* state) {
+                                                       const HGeo h, const Taps taps, const int* state,
+                                                       uint32_t* __restrict__ zero_next) {
     if (state && state[0]) return;
     extern __shared__ __align__(16) float hsm[];
     const int RH = h.RH, TWH = h.TWH, ld = RH + 1;
@@ -82,13 +85,28 @@ __global__ void __launch_bounds__(256) smooth_h_kernel(const T* __restrict__ in,
     const int j0 = blockIdx.y * RH, i0 = blockIdx.x * TWH;
     const int W = TWH + 2 * R;
     const bool interior = i0 - R >= 0 && i0 + TWH + R <= s;
-    for (int q = threadIdx.x; q < RH * W; q += blockDim.x) {
-        const int r = q / W, c = q - r * W;
-        const int col = interior ? i0 - R + c : reflect_index(i0 - R + c, s);
-        sh[c * ld + r] = (float)in[(int64_t)(j0 + r) * s + col];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // warps over rows, lanes over columns: coalesced reads, no index division
+    for (int r = w; r < RH; r += nw) {
+        const T* row = in + (int64_t)(j0 + r) * s;
+        constexpr int U = 4;
+        for (int c0 = lane; c0 < W; c0 += 32 * U) {
+            float v[U];
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                const int c = c0 + 32 * e;
+                if (c < W) v[e] = (float)__ldg(row + (interior ? i0 - R + c : reflect_index(i0 - R + c, s)));
+            }
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                const int c = c0 + 32 * e;
+                if (c < W) sh[c * ld + r] = v[e];
+            }
+        }
+        if (zero_next)
+            for (int c = lane; c < TWH; c += 32) zero_next[(int64_t)(j0 + r) * s + i0 + c] = 0u;
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane < RH) {
         const int c0 = w * h.CW;
         fir_line<R, 8>(
@@ -96,10 +114,8 @@ __global__ void __launch_bounds__(256) smooth_h_kernel(const T* __restrict__ in,
             [&](int p, float v) { so[lane * (TWH + 1) + c0 + p] = v; });
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < RH * TWH; q += blockDim.x) {
-        const int r = q / TWH, c = q - r * TWH;
-        out[(int64_t)(j0 + r) * s + i0 + c] = so[r * (TWH + 1) + c];
-    }
+    for (int r = w; r < RH; r += nw)
+        for (int c = lane; c < TWH; c += 32) out[(int64_t)(j0 + r) * s + i0 + c] = so[r * (TWH + 1) + c];
 }
 
 // -------------------------------------------------------------------------- vertical
@@ -111,12 +127,12 @@ inline VGeo make_vgeo(const Geo& g) {
     VGeo v;
     v.VR = g.s < 64 ? g.s : 64;
     v.VB = v.VR / g.TH;
-    v.GT = g.NW * 32;
+    v.GT = g.TW < 32 ? 32 : g.TW;  // one thread per column per band
     return v;
 }
 
 inline size_t v_smem_bytes(const Geo& g, const VGeo& v, int R) {
-    return ((size_t)(v.VR + 2 * R) * g.TW + (size_t)v.VR * g.TW + (size_t)v.VB * 3 * g.NW * g.TH) * sizeof(float);
+    return ((size_t)(v.VR + 2 * R) * g.TW + (size_t)v.VR * g.TW) * sizeof(float);
 }
 
 template <int R>
@@ -128,17 +144,32 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
     const int TH = g.TH, TW = g.TW, s = g.s, VR = v.VR;
     float* sh = vsm;                                 // [(VR + 2R)][TW]
     float* sd = vsm + (size_t)(VR + 2 * R) * TW;     // [VR][TW]  d for VB bands
-    float* rec = sd + (size_t)VR * TW;               // VB x tile_reduce scratch
     const int x = blockIdx.x;
     const int a0 = blockIdx.y * VR, i0 = x * TW;
     const int H = VR + 2 * R;
     const bool interior = a0 - R >= 0 && a0 + VR + R <= s;
     if ((TW & 3) == 0) {
+        // (TW/4) float4 per row; threads tile (rows x float4 columns) without division
         const int TW4 = TW >> 2;
-        for (int q = threadIdx.x; q < H * TW4; q += blockDim.x) {
-            const int r = q / TW4, c4 = q - r * TW4;
-            const int row = interior ? a0 - R + r : reflect_index(a0 - R + r, s);
-            reinterpret_cast<float4*>(sh)[q] = __ldg(reinterpret_cast<const float4*>(tmp + (int64_t)row * s + i0) + c4);
+        const int cpr = TW4 < (int)blockDim.x ? TW4 : (int)blockDim.x;  // threads per row
+        const int rpp = blockDim.x / cpr;                                // rows per pass
+        const int c4 = threadIdx.x % cpr, r0 = threadIdx.x / cpr;        // once per thread
+        constexpr int U = 4;
+        for (int rb = r0; rb < H; rb += U * rpp) {
+            float4 v4[U];
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                const int r = rb + e * rpp;
+                if (r < H && c4 < TW4) {
+                    const int row = interior ? a0 - R + r : reflect_index(a0 - R + r, s);
+                    v4[e] = __ldg(reinterpret_cast<const float4*>(tmp + (int64_t)row * s + i0) + c4);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                const int r = rb + e * rpp;
+                if (r < H && c4 < TW4) reinterpret_cast<float4*>(sh)[r * TW4 + c4] = v4[e];
+            }
         }
     } else {
         for (int q = threadIdx.x; q < H * TW; q += blockDim.x) {
@@ -160,8 +191,17 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
             });
     }
     __syncthreads();
-    if (emit)
-        tile_reduce(sd + (size_t)grp * TH * TW, rec + (size_t)grp * 3 * g.NW * TH, g, ws, a0 / TH + grp, x, tid);
+    if (emit) {
+        // one warp per band tile of d, straight from shared memory
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+        for (int gb = warp; gb < v.VB; gb += nwarps) {
+            const float* src = sd + (size_t)gb * TH * TW;
+            const int b = a0 / TH + gb;
+            if (g.CPL == 4) warp_tile_reduce<4>(src, TW, g, ws, b, x, lane);
+            else if (g.CPL == 2) warp_tile_reduce<2>(src, TW, g, ws, b, x, lane);
+            else warp_tile_reduce<1>(src, TW, g, ws, b, x, lane);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------- launch
@@ -180,7 +220,8 @@ static void make_taps(int kernel_size, Taps* taps) {
 }
 
 template <int R, typename T>
-static int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, cudaStream_t st) {
+static int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, uint32_t* zero_next,
+                    cudaStream_t st) {
     const HGeo h = make_hgeo(s);
     const size_t smem = h_smem_bytes(h, R);
     static bool attr = false;
@@ -189,7 +230,7 @@ static int launch_h(const T* in, float* out, int s, const Taps& taps, const int*
         attr = true;
     }
     dim3 grid(s / h.TWH, s / h.RH);
-    smooth_h_kernel<R, T><<<grid, h.NWH * 32, smem, st>>>(in, out, s, h, taps, state);
+    smooth_h_kernel<R, T><<<grid, h.NWH * 32, smem, st>>>(in, out, s, h, taps, state, zero_next);
     prof_mark(st, "smooth_h");
     return (int)cudaGetLastError();
 }
@@ -212,23 +253,24 @@ static int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, cons
 
 template <int KS>
 static int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
-                       float* d, int emit, const int* state, cudaStream_t st) {
+                       float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
     constexpr int R = 3 * KS;
-    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, st)
-                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, st);
+    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st)
+                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st);
     if (rc) return rc;
     return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st);
 }
 
 int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
-                        float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st) {
+                        float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
+                        uint32_t* zero_next) {
     if (kernel_size < 1 || 3 * kernel_size > kMaxR) return INIM_EKERNEL;  // 1 <= ks <= 16
     Taps taps;
     make_taps(kernel_size, &taps);
     const int emit = emit_aggregates ? 1 : 0;
     switch (kernel_size) {
 #define INIM_KS(K) \
-    case K: return launch_pair<K>(in, in_is_counts, g, ws, taps, background, d, emit, state, st);
+    case K: return launch_pair<K>(in, in_is_counts, g, ws, taps, background, d, emit, state, zero_next, st);
         INIM_KS(1) INIM_KS(2) INIM_KS(3) INIM_KS(4) INIM_KS(5) INIM_KS(6) INIM_KS(7) INIM_KS(8)
         INIM_KS(9) INIM_KS(10) INIM_KS(11) INIM_KS(12) INIM_KS(13) INIM_KS(14) INIM_KS(15) INIM_KS(16)
 #undef INIM_KS
