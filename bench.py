@@ -61,6 +61,28 @@ def four_cluster(n: int = N_POINTS, seed: int = 4) -> np.ndarray:
     return np.concatenate(parts).astype(np.float32).astype(np.float64)
 
 
+def c3_points(n: int, seed: int = 42) -> np.ndarray:
+    """BASELINE configs[2] input: gaussian mixture of 4-8 clusters, sigma 0.02-0.06
+    (the reference acceptance-test pattern), fp32-representable."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence((seed, n))))
+    m = int(rng.integers(4, 9))
+    w = rng.uniform(0.5, 2.0, size=m)
+    counts = np.floor(w / w.sum() * n).astype(np.int64)
+    counts[: n - int(counts.sum())] += 1
+    centres = rng.uniform(0.12, 0.88, size=(m, 2))
+    sig = rng.uniform(0.02, 0.06, size=m)
+    parts = []
+    for c in range(m):
+        p = rng.normal(centres[c], sig[c], size=(int(counts[c]), 2))
+        for _ in range(64):
+            bad = np.any((p < 0) | (p > 1), axis=1)
+            if not bad.any():
+                break
+            p[bad] = rng.normal(centres[c], sig[c], size=(int(bad.sum()), 2))
+        parts.append(np.clip(p, 0, 1))
+    return np.concatenate(parts).astype(np.float32).astype(np.float64)
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -154,8 +176,11 @@ def bench_ours(args):
 
     lib = _lib.load()
     dev = torch.device("cuda", local)
-    host = four_cluster(N_POINTS, seed=4 + rank)
-    n, k = len(host), K_GRID
+    if args.workload == "c3":
+        host, k = c3_points(16_000_000, seed=42 + rank), 12
+    else:
+        host, k = four_cluster(N_POINTS, seed=4 + rank), K_GRID
+    n = len(host)
     m = 1 << (2 * k)
     pts_in = torch.from_numpy(host.astype(np.float32)).to(dev)
     pts = torch.empty_like(pts_in)
@@ -227,13 +252,15 @@ def bench_ours(args):
     integral = bench_integral(lib, D, dev, flush, sizes=(12,), reps=10)
 
     # -- end to end through the public API with host buffers (pinned), rank-local
-    e2e = bench_e2e(P, host, reps=max(3, min(args.steps, 10)))
+    e2e = bench_e2e(P, host, k, reps=max(3, min(args.steps, 10)))
 
     if rank != 0:
         return
-    cpu = cpu_baseline(host) if world == 1 and not args.no_cpu_baseline else None
+    cpu = cpu_baseline(host, k, iterations=4 if k == K_GRID else 2) \
+        if world == 1 and not args.no_cpu_baseline else None
+    c3 = args.workload == "c3"
     line = {
-        "metric": METRIC,
+        "metric": METRIC if not c3 else "regularization iters/sec (16M pts, 4096² grid)",
         "value": value,
         "unit": "iters/s",
         "n_gpus": world,
@@ -244,8 +271,11 @@ def bench_ours(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic four-cluster (400k/300k/200k/100k, sigma 0.05), fp32-representable",
-        "config": {"workload": "1M pts, 1024^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[1])",
+        "data": ("synthetic gaussian mixture (4-8 clusters, sigma 0.02-0.06), fp32-representable" if c3 else
+                 "synthetic four-cluster (400k/300k/200k/100k, sigma 0.05), fp32-representable"),
+        "config": {"workload": ("16M pts, 4096^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[2])"
+                                if c3 else
+                                "1M pts, 1024^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[1])"),
                    "points": n, "grid": 1 << k, "iterations_per_step": ITERS, "kernel_size": KERNEL_SIZE,
                    "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": f"splom-shard x{world}" if world > 1 else "single plot"},
@@ -303,7 +333,7 @@ def bench_integral(lib, D, dev, flush, sizes=(12,), reps=10):
     return out
 
 
-def bench_e2e(P, host: np.ndarray, reps: int):
+def bench_e2e(P, host: np.ndarray, k: int, reps: int):
     """Same metric through the public drop-in API with host (pinned) buffers: H2D of the
     float64 positions, 10 device iterations, D2H of the final frame, every call."""
     import torch
@@ -312,7 +342,7 @@ def bench_e2e(P, host: np.ndarray, reps: int):
     pinned = torch.empty((n, 2), dtype=torch.float64).pin_memory()
     pinned.numpy()[:] = host
     pos = pinned.numpy()
-    params = P.RegularizationParams(k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS, frame_cap=2)
+    params = P.RegularizationParams(k=k, kernel_size=KERNEL_SIZE, iterations=ITERS, frame_cap=2)
 
     def call():
         r = P.run(P.ScatterDataset(positions=pos), params, store_fields=False)
@@ -328,27 +358,27 @@ def bench_e2e(P, host: np.ndarray, reps: int):
     assert out.shape == (n, 2)
     return {"value": ITERS / dt, "unit": "iters/s", "h2d_bytes_per_step": int(n * 2 * 8),
             "d2h_bytes_per_step": int(n * 2 * 8), "ms_per_call": dt * 1e3,
-            "api": "paper_2408_06513_b200.run(ScatterDataset, RegularizationParams(k=10, kernel_size=8, "
+            "api": f"paper_2408_06513_b200.run(ScatterDataset, RegularizationParams(k={k}, kernel_size=8, "
                    "iterations=10, frame_cap=2), store_fields=False).frame(10)"}
 
 
 # ------------------------------------------------------------------ CPU baseline
-def cpu_baseline(host: np.ndarray, iterations: int = 4):
+def cpu_baseline(host: np.ndarray, k: int = K_GRID, iterations: int = 4):
     """The oracle (C restatement of the reference algorithm, float64) with every host
-    thread, on a bounded sample: `iterations` iterations of the same 1M / 1024^2 input."""
+    thread, on a bounded sample: `iterations` iterations of the same input and grid."""
     from oracle import oracle as O
 
     cores = os.cpu_count() or 1
     O.set_threads(cores)
-    defect = O.flat_response(K_GRID)
+    defect = O.flat_response(k)
     pos = host
     t0 = time.perf_counter()
     for _ in range(iterations):
-        pos = O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
+        pos = O.iterate_once(pos, k, KERNEL_SIZE, None, defect)
     dt = time.perf_counter() - t0
     return {"value": iterations / dt, "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": f"{iterations} iterations of the 1M-point / 1024^2 / ks=8 workload (float64 C port of "
-                      f"the reference algorithm, OpenMP {cores} threads)"}
+            "sample": f"{iterations} iterations of the {len(host)}-point / {1 << k}^2 / ks=8 workload (float64 C "
+                      f"port of the reference algorithm, OpenMP {cores} threads)"}
 
 
 def bench_reference(args):
@@ -385,18 +415,116 @@ def bench_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def bench_splom(args):
+    """BASELINE configs[3]: SPLOM of --plots plots x 500k points, 1024^2, 10 iterations,
+    plots sharded over ranks, concurrent streams per GPU, one NCCL all-gather of the
+    final positions inside the step.  value = plot-iterations per second (whole job)."""
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, gather_results, shard, splom_plot
+
+    cfg = SplomConfig(nplots=args.plots, points=500_000, k=10, kernel_size=8, iterations=ITERS, streams=8)
+    ids = shard(cfg.nplots, world, rank)
+    job = DeviceSplom(cfg, ids)
+    job.load(lambda i: splom_plot(i, cfg.points))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step():
+        res = job.run()
+        if world > 1:
+            gather_results(res, cfg.nplots, world)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step()
+        b.record()
+        b.synchronize()
+        t_ms += a.elapsed_time(b)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.summary()
+    if world > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    if rank != 0:
+        return
+    total_iters = cfg.nplots * ITERS * args.steps
+    value = total_iters / (t_ms / 1e3)
+    line = {
+        "metric": "regularization iters/sec (SPLOM batch, 500k pts per plot, 1024² grid)",
+        "value": value, "unit": "plot-iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic gaussian mixtures (PCG64 seeds (2408, plot))",
+        "config": {"workload": f"SPLOM {cfg.nplots} plots x 500k pts, 1024^2, 10 iterations (BASELINE configs[3])",
+                   "plots": cfg.nplots, "streams_per_gpu": cfg.streams,
+                   "parallelism": f"plots sharded over {world} GPU(s), NCCL all-gather of final positions",
+                   "l2": "flushed between timed steps"},
+        "gpu_launches": int(cfg.nplots * ITERS * args.steps * 9),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_sweep(args):
+    """BASELINE configs[4]: integral-image-only sweep 512^2 .. 16384^2, fp32, L2 flushed."""
+    import torch
+
+    from paper_2408_06513_b200 import _device as D
+    from paper_2408_06513_b200 import _lib
+
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sampler = ClockSampler(0)
+    sampler.start()
+    rows = bench_integral(lib, D, dev, flush, sizes=tuple(range(9, 15)), reps=max(5, args.steps))
+    clocks = sampler.summary()
+    best = max(rows, key=lambda r: r["frac"])
+    line = {"metric": "integral-image GB/s vs HBM peak (36 B/px: read d, write 8 fp32 tables)",
+            "value": best["GB_s"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": 3,
+            "ms_per_step": best["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic uniform random textures",
+            "config": {"workload": "integral-image-only sweep 512^2..16384^2 (BASELINE configs[4])",
+                       "best_size": best["size"]},
+            "sweep": rows, "clocks": clocks}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "splom", "sweep"],
+                    help="c2: 1M pts/1024^2 (headline); c3: 16M pts/4096^2; splom: configs[3]; "
+                         "sweep: integral-only 512^2..16384^2")
+    ap.add_argument("--plots", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         bench_reference(args)
+    elif args.workload == "splom":
+        bench_splom(args)
+    elif args.workload == "sweep":
+        bench_sweep(args)
     else:
         bench_ours(args)
     _rank, world, _ = dist_env()

@@ -1,0 +1,145 @@
+"""Scatterplot-matrix (SPLOM) batches: many independent plots regularized at once
+(BASELINE.json configs[3]: 256 plots x 500k points, 1024^2, 10 iterations).
+
+Plots are independent (no cross-plot term anywhere in the reference's regularize.py:
+40-80), so the batch is partitioned across ranks into contiguous blocks with no
+data-path communication; inside a rank, plots run concurrently on several CUDA streams
+(each stream replays its own captured iteration graph on its own workspace), which
+fills the GPU with the small 1024^2 grid kernels of several plots at once.  One
+collective at the end gathers the final positions of every plot (NCCL all-gather over
+NVLink on GPUs; gloo in the CPU tests).
+
+The reference runs the same workload as a process pool over host cores
+(tests/test_acceptance.py:124-128).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+
+def shard(nplots: int, world: int, rank: int) -> range:
+    """Contiguous block of plot indices owned by `rank` (sizes differ by at most one)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(nplots, world)
+    start = rank * base + min(rank, extra)
+    return range(start, start + base + (1 if rank < extra else 0))
+
+
+def splom_plot(idx: int, n: int, seed: int = 2408) -> np.ndarray:
+    """Synthetic plot `idx` of the batch: a Gaussian mixture of 1-8 clusters (PCG64
+    stream seeded by (seed, idx), the reference suite's seeding pattern,
+    datasets.py:140-149), float32-representable, resampled into [0, 1]^2."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence((seed, idx))))
+    m = int(rng.integers(1, 9))
+    w = rng.uniform(0.5, 2.0, size=m)
+    counts = np.floor(w / w.sum() * n).astype(np.int64)
+    counts[: n - int(counts.sum())] += 1
+    centres = rng.uniform(0.12, 0.88, size=(m, 2))
+    sig = rng.uniform(0.005, 0.02, size=m)
+    parts = []
+    for c in range(m):
+        p = rng.normal(centres[c], sig[c], size=(int(counts[c]), 2))
+        for _ in range(64):
+            bad = np.any((p < 0) | (p > 1), axis=1)
+            if not bad.any():
+                break
+            p[bad] = rng.normal(centres[c], sig[c], size=(int(bad.sum()), 2))
+        parts.append(np.clip(p, 0, 1))
+    return np.concatenate(parts).astype(np.float32).astype(np.float64)
+
+
+@dataclass
+class SplomConfig:
+    nplots: int = 256
+    points: int = 500_000
+    k: int = 10
+    kernel_size: int = 8
+    iterations: int = 10
+    streams: int = 8
+
+
+class DeviceSplom:
+    """Runs this rank's block of plots on `streams` concurrent CUDA streams."""
+
+    def __init__(self, cfg: SplomConfig, plot_ids: Sequence[int], device=None):
+        import torch
+
+        from . import _device as D
+        from . import _lib
+
+        self.torch, self.D, self._lib = torch, D, _lib
+        self.lib = D.require_cuda()
+        self.cfg = cfg
+        self.ids = list(plot_ids)
+        self.dev = device or D.device()
+        n = cfg.points
+        self.inputs = torch.empty((len(self.ids), n, 2), dtype=torch.float32, device=self.dev)
+        self.work = torch.empty_like(self.inputs)
+        nst = max(1, min(cfg.streams, len(self.ids)))
+        self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(nst)]
+        wsb = int(self.lib.inim_workspace_bytes(cfg.k, n))
+        self.ws = [torch.empty(wsb, dtype=torch.uint8, device=self.dev) for _ in range(nst)]
+
+    def load(self, make_plot: Callable[[int], np.ndarray]):
+        for q, idx in enumerate(self.ids):
+            self.inputs[q].copy_(self.torch.from_numpy(make_plot(idx).astype(np.float32)))
+
+    def run(self):
+        """All plots, `iterations` each; inputs stay untouched (results in .work)."""
+        torch, D, lib, cfg = self.torch, self.D, self.lib, self.cfg
+        cur = torch.cuda.current_stream(self.dev)
+        start = torch.cuda.Event()
+        start.record(cur)
+        for st in self.streams:
+            st.wait_event(start)
+        for q in range(len(self.ids)):
+            si = q % len(self.streams)
+            st = self.streams[si]
+            with torch.cuda.stream(st):
+                self.work[q].copy_(self.inputs[q])
+                self._lib.check(lib.inim_run(D.ptr(self.work[q]), cfg.points, cfg.k, cfg.kernel_size, 0.0,
+                                             cfg.iterations, 0.0, None, None, None, None, None,
+                                             D.ptr(self.ws[si]), st.cuda_stream), "splom run")
+        for st in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(st)
+            cur.wait_event(ev)
+        return self.work
+
+
+def gather_results(local, nplots: int, world: int, group=None):
+    """All-gather every rank's block of final positions into (nplots, n, 2) on every
+    rank.  Blocks are padded to the largest shard so one all_gather_into_tensor moves
+    everything; padding rows are dropped afterwards."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return local
+    per = max(len(shard(nplots, world, r)) for r in range(world))
+    shape = (per,) + tuple(local.shape[1:])
+    buf = torch.zeros(shape, dtype=local.dtype, device=local.device)
+    buf[: local.shape[0]].copy_(local)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world,) + shape, dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(out, buf, group=group)  # one NCCL all-gather over NVLink
+        blocks = [out[r] for r in range(world)]
+    else:  # gloo (CPU tests): list form
+        blocks = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(blocks, buf, group=group)
+    parts = [blocks[r][: len(shard(nplots, world, r))] for r in range(world)]
+    return torch.cat(parts, dim=0)
+
+
+def run_distributed(cfg: SplomConfig, rank: int, world: int, make_plot: Optional[Callable] = None, group=None):
+    """One rank's share of the batch + the gather; returns all final positions."""
+    ids = shard(cfg.nplots, world, rank)
+    job = DeviceSplom(cfg, ids)
+    job.load(make_plot or (lambda i: splom_plot(i, cfg.points)))
+    res = job.run()
+    return gather_results(res, cfg.nplots, world, group)

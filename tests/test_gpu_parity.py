@@ -386,3 +386,28 @@ def test_run_host_abi_end_to_end(P, oracle):
     assert rc == 0
     want = oracle.run_positions(pts, 8, 8, 3)[-1]
     assert maxerr(out, want) <= POS_TOL
+
+
+def test_splom_streams_match_single_plot_runs(P):
+    """SPLOM batch on concurrent streams == each plot regularized alone (bit-identical)."""
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
+
+    cfg = SplomConfig(nplots=6, points=20_000, k=8, kernel_size=8, iterations=4, streams=3)
+    job = DeviceSplom(cfg, range(cfg.nplots))
+    job.load(lambda i: splom_plot(i, cfg.points))
+    res = job.run().cpu().numpy().astype(np.float64)
+    for i in range(cfg.nplots):
+        r = P.run(P.ScatterDataset(positions=splom_plot(i, cfg.points)),
+                  P.RegularizationParams(k=8, kernel_size=8, iterations=4), store_fields=False)
+        assert np.array_equal(res[i], r.frame(4)), i
+
+
+@pytest.mark.parametrize("k", [11, 12])
+def test_larger_grids_run_against_oracle(P, oracle, k):
+    """2048^2 and 4096^2 grids (BASELINE configs[2] grid size), 2 iterations."""
+    pts = clusters(400_000, k)
+    frames = oracle.run_positions(pts, k, 8, 2)
+    r = P.run(P.ScatterDataset(positions=pts), P.RegularizationParams(k=k, kernel_size=8, iterations=2),
+              store_fields=False)
+    for t in range(3):
+        assert maxerr(r.frame(t), frames[t]) <= POS_TOL, t
