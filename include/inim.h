@@ -163,6 +163,14 @@ int inim_run_uncached(float* pts, int64_t n, int k, int kernel_size, float backg
                       float stop_eps, float* frames, float* fields, float* disp, float* excursions, int* state,
                       void* ws, cudaStream_t stream);
 
+/* The persistent single-launch run (used by inim_run for 64^2..2048^2 grids with
+ * kernel_size 8) with %globaltimer stamps written to stamps_dev (device, >= 16 u64) at
+ * every phase boundary of the first iteration: splat, smooth_h, smooth_v+reduce,
+ * band_rows, colscan, diagscan, marg, field, move.  Returns 1 if the persistent path
+ * ran, 0 if this configuration uses the graph of standalone kernels, < 0 on error. */
+int inim_run_stamped(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, void* ws,
+                     cudaStream_t stream, unsigned long long* stamps_dev);
+
 /* Profiling: `iterations` iterations launched eagerly with a CUDA event recorded after
  * every launch; synchronises.  ms_out[q] = duration of launch q, names_out = the
  * launch names joined by '\n'.  Returns the number of launches (>= 0) or an error. */

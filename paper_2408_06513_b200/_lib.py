@@ -55,7 +55,8 @@ _SIGS = {
     "inim_run_uncached": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_float, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "inim_clear_graph_cache": (None, []),
-    "inim_profile_run": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_void_p, c_void_p, c_void_p, c_int,
+    "inim_run_stamped": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_void_p, c_void_p, c_void_p]),
+    "inim_profile_run":(c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_void_p, c_void_p, c_void_p, c_int,
                                  ctypes.c_char_p, c_int]),
     "inim_run_host": (c_int, [c_void_p, c_void_p, c_i64, c_int, c_int, c_double, c_int]),
     "inim_kernels_per_iteration": (c_int, [c_int]),

@@ -30,6 +30,24 @@ int cell_count(int k);
 int launch_sort_points(const float* pts, int64_t n, int k, int* hist, int* rank, float* sorted, int* perm,
                        cudaStream_t st);
 int launch_unpermute(const float* sorted, const int* perm, int64_t n, float* out, cudaStream_t st);
+bool mega_supported(const Geo& g, int kernel_size);
+int launch_mega(const Geo& g, const Ws& ws, int kernel_size, float bg, float eps, int iters, float* pts, float* pong,
+                int64_t n, uint32_t* counts, float* d, float* targets, const float* defect, float* frames,
+                float* fields, float* disp, float* excs, float* scratch, int* state, unsigned long long* stamps,
+                cudaStream_t st);
+
+// The persistent single-launch iteration (mega.cu) is opt-in (INIM_MEGA=1): measured
+// per phase it is not yet faster than the graph of standalone kernels, whose kernels
+// run at higher occupancy.
+static bool use_mega(const Geo& g, int ks) {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("INIM_MEGA");
+        env = (e && e[0] == '1') ? 1 : 0;
+    }
+    return env && !g_prof && mega_supported(g, ks);
+}
+static unsigned long long* g_stamps = nullptr;  // set by inim_run_stamped
 
 // Per-iteration bookkeeping for the displacement criterion (regularize.py:76-79).
 __global__ void iter_end_kernel(const float* disp, float eps, int* state) {
@@ -160,6 +178,9 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     }
     const size_t pbytes = sizeof(float) * 2 * (size_t)key.n;
     if (frames && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(frames, pts, pbytes, cudaMemcpyDeviceToDevice, st));
+    if (key.n > 0 && use_mega(g, key.ks))  // the whole run in one persistent launch
+        return launch_mega(g, w, key.ks, key.bg, key.eps, key.iters, pts, sortB, key.n, counts, d, tg_scratch, defect,
+                           frames, fields, disp, excursions, scratch, state, g_stamps, st);
     // Optional spatial pre-sort of the points (kSortPoints): a single counting sort by
     // cell; off until its hot-cell atomics are privatised (it currently costs more than
     // the gathers it saves).
@@ -346,6 +367,23 @@ int inim_iterate(const float* pts_in, float* pts_out, int64_t n, int k, int kern
                              stream);
 }
 
+int inim_run_stamped(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, void* ws,
+                     cudaStream_t stream, unsigned long long* stamps_dev) {
+    // The persistent path with %globaltimer stamps at every phase boundary of the first
+    // iteration (device buffer of >= 16 u64); returns 1 if the persistent path ran.
+    if (k < 1 || k > INIM_MAX_K || n <= 0 || iterations < 1 || !ws || !pts || !stamps_dev) return INIM_EINVAL;
+    const Geo g = make_geo(k);
+    if (!use_mega(g, kernel_size)) return 0;
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations;
+    g_stamps = stamps_dev;
+    const int rc = enqueue_run(key, pts, nullptr, nullptr, nullptr, nullptr, nullptr, ws, stream);
+    g_stamps = nullptr;
+    return rc ? rc : 1;
+}
+
 int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
              float* frames, float* fields, float* disp, float* excursions, int* state, void* ws, cudaStream_t stream) {
     if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
@@ -357,6 +395,8 @@ int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, in
     key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
     key.iters = iterations; key.eps = stop_eps; key.frames = frames; key.fields = fields; key.disp = disp;
     key.exc = excursions; key.state = state; key.ws = ws; key.st = stream;
+    if (n > 0 && use_mega(make_geo(k), kernel_size))  // a handful of launches: no graph needed
+        return enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
     {
         std::lock_guard<std::mutex> lock(g_mu);
         for (auto& e : g_cache)

@@ -1,0 +1,209 @@
+// Smoothing tile functions (gaussian_smooth + background, reference density.py:30-78),
+// shared by the standalone smoothing kernels (smooth.cu) and the persistent iteration
+// kernel (mega.cu).  Each function processes one tile with the whole CTA and contains
+// CTA-wide barriers, so every thread of the CTA must call it.
+#pragma once
+
+#include "inim_tiles.cuh"
+
+namespace inim {
+
+constexpr int kMaxR = 48;  // kernel_size <= 16
+
+struct Taps {
+    float w[2 * kMaxR + 1];
+};
+
+// out[p] = sum_{t=0}^{2R} w[t] * line(p + t),  p in [0, n).  Register-blocked: P partial
+// outputs per thread, every input read once per P outputs; taps are constant-bank
+// operands of FFMA.
+template <int R, int P, typename Load, typename Store>
+__device__ __forceinline__ void fir_line(const Taps& taps, int n, Load line, Store store) {
+    constexpr int NT = 2 * R + 1;
+    int p0 = 0;
+    for (; p0 + P <= n; p0 += P) {
+        float acc[P];
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) acc[pp] = 0.f;
+#pragma unroll
+        for (int q = 0; q < P + NT - 1; ++q) {
+            const float v = line(p0 + q);
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) {
+                const int t = q - pp;
+                if (t >= 0 && t < NT) acc[pp] = fmaf(taps.w[t], v, acc[pp]);
+            }
+        }
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) store(p0 + pp, acc[pp]);
+    }
+    for (; p0 < n; ++p0) {
+        float acc = 0.f;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc = fmaf(taps.w[t], line(p0 + t), acc);
+        store(p0, acc);
+    }
+}
+
+// ------------------------------------------------------------------------ horizontal
+// Tile: RH rows x TWH columns; lane = row, warp = a CW-wide column chunk.
+struct HGeo {
+    int RH, TWH, NWH, CW;
+};
+
+inline HGeo make_hgeo(int s) {
+    HGeo h;
+    h.RH = s < 32 ? s : 32;
+    h.TWH = s < 128 ? s : 128;
+    int nw = h.TWH / 16;
+    h.NWH = nw < 1 ? 1 : (nw > 8 ? 8 : nw);
+    h.CW = h.TWH / h.NWH;
+    return h;
+}
+
+__host__ __device__ inline size_t h_smem_bytes(const HGeo& h, int R) {
+    return ((size_t)(h.TWH + 2 * R) * (h.RH + 1) + (size_t)h.RH * (h.TWH + 1)) * sizeof(float);
+}
+
+// Horizontal pass of tile (bx, by).  zero_next (optional): the other count buffer of
+// the iteration's ping-pong pair; the tile clears its own RH x TWH block of it.
+template <int R, typename T>
+__device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* __restrict__ out, int s, const HGeo& h,
+                                              const Taps& taps, uint32_t* __restrict__ zero_next, int bx, int by,
+                                              float* hsm) {
+    const int RH = h.RH, TWH = h.TWH, ld = RH + 1;
+    float* sh = hsm;                                 // [(TWH + 2R)][RH + 1]  transposed input
+    float* so = hsm + (size_t)(TWH + 2 * R) * ld;    // [RH][TWH + 1]          output staging
+    const int j0 = by * RH, i0 = bx * TWH;
+    const int W = TWH + 2 * R;
+    const bool interior = i0 - R >= 0 && i0 + TWH + R <= s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // warps over rows, lanes over columns (coalesced, no index division); every load of
+    // a pass is issued before any of its shared-memory stores (up to RPW x NPR loads in
+    // flight per thread)
+    constexpr int RPW = 4;                    // rows per warp per pass
+    constexpr int NPR = (128 + 2 * R + 31) / 32;  // columns per lane per row (TWH <= 128)
+    for (int r0 = w; r0 < RH; r0 += RPW * nw) {
+        T v[RPW][NPR];
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+            const int r = r0 + q * nw;
+            const T* row = in + (int64_t)(j0 + (r < RH ? r : 0)) * s;
+#pragma unroll
+            for (int e = 0; e < NPR; ++e) {
+                const int c = lane + 32 * e;
+                if (r < RH && c < W) v[q][e] = __ldg(row + (interior ? i0 - R + c : reflect_index(i0 - R + c, s)));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RPW; ++q) {
+            const int r = r0 + q * nw;
+#pragma unroll
+            for (int e = 0; e < NPR; ++e) {
+                const int c = lane + 32 * e;
+                if (r < RH && c < W) sh[c * ld + r] = (float)v[q][e];
+            }
+            if (zero_next && r < RH)
+                for (int c = lane; c < TWH; c += 32) zero_next[(int64_t)(j0 + r) * s + i0 + c] = 0u;
+        }
+    }
+    __syncthreads();
+    if (lane < RH && w < h.NWH) {
+        const int c0 = w * h.CW;
+        fir_line<R, 8>(
+            taps, h.CW, [&](int q) { return sh[(c0 + q) * ld + lane]; },
+            [&](int p, float v) { so[lane * (TWH + 1) + c0 + p] = v; });
+    }
+    __syncthreads();
+    for (int r = w; r < RH; r += nw)
+        for (int c = lane; c < TWH; c += 32) out[(int64_t)(j0 + r) * s + i0 + c] = so[r * (TWH + 1) + c];
+    __syncthreads();  // the tile's shared memory may be reused by the caller's next tile
+}
+
+// -------------------------------------------------------------------------- vertical
+struct VGeo {
+    int VR, VB, GT;  // rows per CTA, bands per CTA, threads per band group
+};
+
+inline VGeo make_vgeo(const Geo& g) {
+    VGeo v;
+    v.VR = g.s < 64 ? g.s : 64;
+    v.VB = v.VR / g.TH;
+    v.GT = g.TW < 32 ? 32 : g.TW;  // one thread per column per band
+    return v;
+}
+
+__host__ __device__ inline size_t v_smem_bytes(const Geo& g, const VGeo& v, int R) {
+    return ((size_t)(v.VR + 2 * R) * g.TW + (size_t)v.VR * g.TW) * sizeof(float);
+}
+
+// Vertical pass + background of tile (bx, by) = VB bands x TW columns; with `emit`,
+// each band's tile of d goes straight from shared memory into the tile reduce.
+template <int R>
+__device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, float* __restrict__ d, const Geo& g,
+                                              const VGeo& v, const Ws& ws, const Taps& taps, float background,
+                                              int emit, int bx, int by, float* vsm) {
+    const int TH = g.TH, TW = g.TW, s = g.s, VR = v.VR;
+    float* sh = vsm;                                 // [(VR + 2R)][TW]
+    float* sd = vsm + (size_t)(VR + 2 * R) * TW;     // [VR][TW]  d for VB bands
+    const int x = bx;
+    const int a0 = by * VR, i0 = x * TW;
+    const int H = VR + 2 * R;
+    const bool interior = a0 - R >= 0 && a0 + VR + R <= s;
+    if ((TW & 3) == 0) {
+        // (TW/4) float4 per row; threads tile (rows x float4 columns) without division
+        const int TW4 = TW >> 2;
+        const int cpr = TW4 < (int)blockDim.x ? TW4 : (int)blockDim.x;  // threads per row
+        const int rpp = blockDim.x / cpr;                                // rows per pass
+        const int c4 = threadIdx.x % cpr, r0 = threadIdx.x / cpr;
+        constexpr int U = 4;
+        for (int rb = r0; rb < H; rb += U * rpp) {
+            float4 v4[U];
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                const int r = rb + e * rpp;
+                if (r < H && c4 < TW4) {
+                    const int row = interior ? a0 - R + r : reflect_index(a0 - R + r, s);
+                    v4[e] = __ldg(reinterpret_cast<const float4*>(tmp + (int64_t)row * s + i0) + c4);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < U; ++e) {
+                const int r = rb + e * rpp;
+                if (r < H && c4 < TW4) reinterpret_cast<float4*>(sh)[r * TW4 + c4] = v4[e];
+            }
+        }
+    } else {
+        for (int q = threadIdx.x; q < H * TW; q += blockDim.x) {
+            const int r = q / TW, c = q - r * TW;
+            sh[q] = tmp[(int64_t)reflect_index(a0 - R + r, s) * s + i0 + c];
+        }
+    }
+    __syncthreads();
+    const int grp = threadIdx.x / v.GT, tid = threadIdx.x - grp * v.GT;
+    if (grp < v.VB && tid < TW) {
+        const int rb = grp * TH;  // first row of this group's band within the CTA
+        fir_line<R, 8>(
+            taps, TH, [&](int q) { return sh[(rb + q) * TW + tid]; },
+            [&](int p, float val) {
+                const float dv = val + background;
+                sd[(rb + p) * TW + tid] = dv;
+                d[(int64_t)(a0 + rb + p) * s + i0 + tid] = dv;
+            });
+    }
+    __syncthreads();
+    if (emit) {
+        // one warp per band tile of d, straight from shared memory
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+        for (int gb = warp; gb < v.VB; gb += nwarps) {
+            const float* src = sd + (size_t)gb * TH * TW;
+            const int b = a0 / TH + gb;
+            if (g.CPL == 4) warp_tile_reduce<4>(src, TW, g, ws, b, x, lane);
+            else if (g.CPL == 2) warp_tile_reduce<2>(src, TW, g, ws, b, x, lane);
+            else warp_tile_reduce<1>(src, TW, g, ws, b, x, lane);
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace inim

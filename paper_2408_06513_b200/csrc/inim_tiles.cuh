@@ -236,7 +236,26 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
 #pragma unroll
     for (int e = 0; e < CPL; ++e) V[e] = UL[e] = UR[e] = 0.f;
     float exc = 0.f;
+    // MODE 1 with a precomputed flat response: the row's defect values are fetched one
+    // row ahead so their latency hides behind the previous row's work.
+    const float2* defrow = (MODE == 1 && out.defect && act)
+                               ? reinterpret_cast<const float2*>(out.defect) + (int64_t)a * s + i0 + u0
+                               : nullptr;
+    float2 dnext[CPL];
+    if (defrow) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) dnext[e] = __ldg(defrow + e);
+    }
     for (int r = 0; r < TH; ++r) {
+        float2 dcur[CPL];
+        if (defrow) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) dcur[e] = dnext[e];
+            if (r + 1 < TH) {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) dnext[e] = __ldg(defrow + (int64_t)(r + 1) * s + e);
+            }
+        }
         float dv[CPL];
         if (act) load_row<CPL>(src + (size_t)r * ld + u0, dv);
         else {
@@ -310,7 +329,10 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                 const double tx = (tl * (1.0 - 2.0 * yy) + up * (2.0 * xx - 1.0) + Gx) * inv;
                 const double ty = (tl * (1.0 - 2.0 * xx) + up * (1.0 - 2.0 * yy) + Gy) * inv;
                 double2 def;
-                if (out.defect) {
+                if (defrow) {
+                    def.x = dcur[e].x;
+                    def.y = dcur[e].y;
+                } else if (out.defect) {
                     const float2 dfv = reinterpret_cast<const float2*>(out.defect)[(int64_t)j * s + i];
                     def.x = dfv.x;
                     def.y = dfv.y;

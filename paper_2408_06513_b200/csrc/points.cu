@@ -2,19 +2,9 @@
 // model.py:189-198) and the bilinear move (mapping.py:207-246 + the clip of
 // regularize.py:36).  Both stream the (n, 2) interleaved positions with 16-byte
 // vector accesses (two points per float4) and touch the grid through L2.
-#include "inim_internal.cuh"
+#include "inim_points.cuh"
 
 namespace inim {
-
-template <typename T>
-__device__ __forceinline__ int pixel_of(T v, int s) {
-    // i = min(floor(v * s), s - 1); v * s is exact for s = 2^k, so float32 and
-    // float64 coordinates bin identically when the values are identical.
-    const T f = floor(v * (T)s);
-    int i = (int)f;
-    i = i > s - 1 ? s - 1 : i;
-    return i < 0 ? 0 : i;
-}
 
 // Warp-aggregated integer atomics: lanes hitting the same pixel in one step are
 // merged (__match_any_sync) and the leader issues one red.add for the group.
@@ -66,32 +56,6 @@ __global__ void __launch_bounds__(256) splat_f64_kernel(const double* __restrict
     }
 }
 
-// _bilinear_kernel (mapping.py:207-232): i0 = clamp(floor(x*s), 0, s-2), fx = x*s - i0
-// (in [1, 2] on the last strip: one-sided extrapolation keeps an identity field the
-// identity), then the four-tap blend, then the clip of regularize.py:36.
-template <typename T>
-__device__ __forceinline__ void bilinear(const float2* __restrict__ tg, int s, T x, T y, T& ox, T& oy) {
-    const T sx = x * (T)s, sy = y * (T)s;
-    int i0 = (int)floor(sx), j0 = (int)floor(sy);
-    i0 = i0 < 0 ? 0 : (i0 > s - 2 ? s - 2 : i0);
-    j0 = j0 < 0 ? 0 : (j0 > s - 2 ? s - 2 : j0);
-    const T fx = sx - (T)i0, fy = sy - (T)j0;
-    const T w00 = ((T)1 - fx) * ((T)1 - fy);
-    const T w10 = fx * ((T)1 - fy);
-    const T w01 = ((T)1 - fx) * fy;
-    const T w11 = fx * fy;
-    const int64_t base = (int64_t)j0 * s + i0;
-    const float2 t00 = __ldg(tg + base), t10 = __ldg(tg + base + 1);
-    const float2 t01 = __ldg(tg + base + s), t11 = __ldg(tg + base + s + 1);
-    ox = w00 * (T)t00.x + w10 * (T)t10.x + w01 * (T)t01.x + w11 * (T)t11.x;
-    oy = w00 * (T)t00.y + w10 * (T)t10.y + w01 * (T)t01.y + w11 * (T)t11.y;
-}
-
-template <typename T>
-__device__ __forceinline__ T clip01(T v) {
-    return v < (T)0 ? (T)0 : (v > (T)1 ? (T)1 : v);
-}
-
 __global__ void __launch_bounds__(256) sample_f32_kernel(const float2* __restrict__ tg, int k,
                                                          const float4* __restrict__ in2, const float* __restrict__ in,
                                                          float4* __restrict__ out2, float* __restrict__ out, int64_t n,
@@ -101,20 +65,33 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float2* __restric
     const int64_t npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     float md = 0.f;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
-        const float4 v = __ldcs(in2 + p);
-        float4 o;
+    // four points (two 16-byte loads) per thread per step: 16 independent gathers in flight
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += 2 * stride) {
+        const int64_t p1 = p0 + stride;
+        const bool has1 = p1 < npair;
+        const float4 v0 = __ldcs(in2 + p0);
+        const float4 v1 = has1 ? __ldcs(in2 + p1) : v0;
+        float4 o0, o1;
         if (stopped) {
-            o = v;  // keep the ping-pong buffers consistent after a displacement stop
+            o0 = v0;  // keep the ping-pong buffers consistent after a displacement stop
+            o1 = v1;
         } else {
-            bilinear<float>(tg, s, v.x, v.y, o.x, o.y);
-            bilinear<float>(tg, s, v.z, v.w, o.z, o.w);
+            bilinear<float>(tg, s, v0.x, v0.y, o0.x, o0.y);
+            bilinear<float>(tg, s, v0.z, v0.w, o0.z, o0.w);
+            bilinear<float>(tg, s, v1.x, v1.y, o1.x, o1.y);
+            bilinear<float>(tg, s, v1.z, v1.w, o1.z, o1.w);
             if (clip) {
-                o.x = clip01(o.x); o.y = clip01(o.y); o.z = clip01(o.z); o.w = clip01(o.w);
+                o0.x = clip01(o0.x); o0.y = clip01(o0.y); o0.z = clip01(o0.z); o0.w = clip01(o0.w);
+                o1.x = clip01(o1.x); o1.y = clip01(o1.y); o1.z = clip01(o1.z); o1.w = clip01(o1.w);
             }
-            md = fmaxf(md, fmaxf(fmaxf(fabsf(o.x - v.x), fabsf(o.y - v.y)), fmaxf(fabsf(o.z - v.z), fabsf(o.w - v.w))));
+            md = fmaxf(md, fmaxf(fmaxf(fabsf(o0.x - v0.x), fabsf(o0.y - v0.y)),
+                                 fmaxf(fabsf(o0.z - v0.z), fabsf(o0.w - v0.w))));
+            if (has1)
+                md = fmaxf(md, fmaxf(fmaxf(fabsf(o1.x - v1.x), fabsf(o1.y - v1.y)),
+                                     fmaxf(fabsf(o1.z - v1.z), fabsf(o1.w - v1.w))));
         }
-        __stcs(out2 + p, o);
+        __stcs(out2 + p0, o0);
+        if (has1) __stcs(out2 + p1, o1);
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const float x = in[2 * (n - 1)], y = in[2 * (n - 1) + 1];
@@ -148,24 +125,65 @@ __global__ void __launch_bounds__(256) sample_f64_kernel(const float2* __restric
 }
 
 // ---------------------------------------------------------------- spatial point order
-// A counting sort of the points by 16 x 16-pixel cell, done once per run: consecutive
-// points (one warp) then fall in the same few cells, so the splat's atomics aggregate
-// and the bilinear gathers hit L1.  No result depends on the order (integer counts,
-// independent per-point moves); frames are scattered back through `perm`.
-constexpr int kCellShift = 4;
+// A counting sort of the points by cell (a 2^cs x 2^cs grid of cells, at most 64 per
+// side), done once per run: consecutive points (one warp) then fall in the same cell, so
+// the bilinear gathers hit L1 and the splat's atomics share addresses.  Both passes
+// privatise the histogram in shared memory (one CTA per contiguous chunk of points), so
+// hot cells of clustered data cost one global atomic per CTA, not one per point.  No
+// result depends on the order (integer counts, independent per-point moves); frames are
+// scattered back through `perm`.
+__host__ __device__ inline int cells_log2(int k) { return k < 6 ? k : 6; }
 
 __device__ __forceinline__ int cell_of(float x, float y, int k) {
     const int s = 1 << k;
-    const int cs = k > kCellShift ? k - kCellShift : 0;  // log2(cells per side)
+    const int cs = cells_log2(k);
     const int sh = k - cs;
     return (pixel_of(y, s) >> sh) * (1 << cs) + (pixel_of(x, s) >> sh);
 }
 
-__global__ void __launch_bounds__(256) cell_count_kernel(const float2* __restrict__ pts, int64_t n, int k,
-                                                         int* __restrict__ hist, int* __restrict__ rank) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+// pass 1: per-CTA shared-memory histogram of its chunk, flushed with one atomic per bin
+__global__ void __launch_bounds__(256) cell_hist_kernel(const float2* __restrict__ pts, int64_t n, int k,
+                                                        int* __restrict__ hist, int ncells, int64_t chunk) {
+    extern __shared__ int cnt[];
+    for (int i = threadIdx.x; i < ncells; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t p0 = (int64_t)blockIdx.x * chunk, p1 = min(n, p0 + chunk);
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
         const float2 v = pts[p];
-        rank[p] = atomicAdd(hist + cell_of(v.x, v.y, k), 1);
+        atomicAdd(cnt + cell_of(v.x, v.y, k), 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncells; i += blockDim.x)
+        if (cnt[i]) atomicAdd(hist + i, cnt[i]);
+}
+
+// pass 2: the CTA reserves one contiguous block per bin (one atomic each), then places
+// its points with shared-memory cursors
+__global__ void __launch_bounds__(256) cell_place_kernel(const float2* __restrict__ pts, int64_t n, int k,
+                                                         int* __restrict__ cursor, int ncells, int64_t chunk,
+                                                         float2* __restrict__ sorted, int* __restrict__ perm) {
+    extern __shared__ int sm[];
+    int* cnt = sm;
+    int* base = sm + ncells;
+    for (int i = threadIdx.x; i < ncells; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t p0 = (int64_t)blockIdx.x * chunk, p1 = min(n, p0 + chunk);
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const float2 v = pts[p];
+        atomicAdd(cnt + cell_of(v.x, v.y, k), 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncells; i += blockDim.x) {
+        base[i] = cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0;
+        cnt[i] = 0;
+    }
+    __syncthreads();
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const float2 v = pts[p];
+        const int c = cell_of(v.x, v.y, k);
+        const int slot = base[c] + atomicAdd(cnt + c, 1);
+        sorted[slot] = v;
+        perm[slot] = (int)p;
     }
 }
 
@@ -201,17 +219,6 @@ __global__ void __launch_bounds__(1024) cell_scan_kernel(int* __restrict__ hist,
         if (i < ncells) hist[i] = carry + sh[w] + inc - v;
         carry += sh[32];
         __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(256) cell_scatter_kernel(const float2* __restrict__ pts, int64_t n, int k,
-                                                           const int* __restrict__ offs, const int* __restrict__ rank,
-                                                           float2* __restrict__ sorted, int* __restrict__ perm) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        const float2 v = pts[p];
-        const int dst = offs[cell_of(v.x, v.y, k)] + rank[p];
-        sorted[dst] = v;
-        perm[dst] = (int)p;
     }
 }
 
@@ -259,21 +266,22 @@ int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const
     return (int)cudaGetLastError();
 }
 
-int cell_count(int k) {
-    const int cs = k > kCellShift ? k - kCellShift : 0;
-    return 1 << (2 * cs);
-}
+int cell_count(int k) { return 1 << (2 * cells_log2(k)); }
 
-// hist: cell_count(k) ints (zeroed here); rank, perm: n ints; sorted: n float2.
+// hist: cell_count(k) ints (zeroed here, then the cursors); perm: n ints; sorted: n
+// float2.  `rank` is unused (kept for the workspace layout).
 int launch_sort_points(const float* pts, int64_t n, int k, int* hist, int* rank, float* sorted, int* perm,
                        cudaStream_t st) {
+    (void)rank;
     const int nc = cell_count(k);
     INIM_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * nc, st));
-    const unsigned grid = grid_for(n > 0 ? n : 1, 256);
-    cell_count_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(pts), n, k, hist, rank);
+    const int ctas = sm_count() * 2;
+    const int64_t chunk = (n + ctas - 1) / ctas;
+    const float2* p2 = reinterpret_cast<const float2*>(pts);
+    cell_hist_kernel<<<ctas, 256, sizeof(int) * nc, st>>>(p2, n, k, hist, nc, chunk);
     cell_scan_kernel<<<1, 1024, 0, st>>>(hist, nc);
-    cell_scatter_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float2*>(pts), n, k, hist, rank,
-                                              reinterpret_cast<float2*>(sorted), perm);
+    cell_place_kernel<<<ctas, 256, 2 * sizeof(int) * nc, st>>>(p2, n, k, hist, nc, chunk,
+                                                               reinterpret_cast<float2*>(sorted), perm);
     prof_mark(st, "sort_points");
     return (int)cudaGetLastError();
 }
