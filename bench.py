@@ -280,7 +280,7 @@ def bench_ours(args):
                    "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": f"splom-shard x{world}" if world > 1 else "single plot"},
         "e2e": e2e,
-        "gpu_launches": int(args.steps * ITERS * lib.inim_kernels_per_iteration(k)),
+        "gpu_launches": int(args.steps * (ITERS * lib.inim_kernels_per_iteration(k) + 1)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": None,
                      "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": kernels[dom]["avg_us"],
@@ -474,7 +474,7 @@ def bench_splom(args):
                    "plots": cfg.nplots, "streams_per_gpu": cfg.streams,
                    "parallelism": f"plots sharded over {world} GPU(s), NCCL all-gather of final positions",
                    "l2": "flushed between timed steps"},
-        "gpu_launches": int(cfg.nplots * ITERS * args.steps * 9),
+        "gpu_launches": int(cfg.nplots * args.steps * (ITERS * 7 + 1)),
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

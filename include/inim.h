@@ -187,7 +187,8 @@ void inim_clear_graph_cache(void);
 int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, int kernel_size, double background,
                   int iterations);
 
-/* Number of kernels inim_iterate launches (for launch accounting). */
+/* Kernels per iteration of inim_run in steady state (launch accounting); a run adds
+ * one splat kernel (the move of iteration t splats iteration t+1). */
 int inim_kernels_per_iteration(int k);
 
 #ifdef __cplusplus

@@ -14,7 +14,8 @@ int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const
                      float* zero0 = nullptr, float* zero1 = nullptr);
 int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cudaStream_t st);
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
-                      const int* state, cudaStream_t st);
+                      const int* state, cudaStream_t st, bool pairs = false, uint32_t* splat_next = nullptr,
+                      float* zn0 = nullptr, float* zn1 = nullptr);
 int launch_sample_f64(const float* tg, int k, const double* in, double* out, int64_t n, int clip, cudaStream_t st);
 int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_t st);
 int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st);
@@ -65,7 +66,9 @@ struct FullLayout {
     size_t counts, d, targets, defect, scratch, sortA, sortB, perm, rank, hist, bytes;
 };
 
-static bool precomputed_defect(const Geo& g) { return g.s <= 2048; }
+// The field kernel folds the closed-form flat response into its normalised arithmetic,
+// so the run loop keeps no defect array.
+static bool precomputed_defect(const Geo&) { return false; }
 
 static FullLayout full_layout(const Geo& g, int64_t n) {
     FullLayout F;
@@ -78,7 +81,7 @@ static FullLayout full_layout(const Geo& g, int64_t n) {
     };
     F.counts = take(sizeof(uint32_t) * 2 * g.m);
     F.d = take(sizeof(float) * g.m);
-    F.targets = take(sizeof(float) * 2 * g.m);
+    F.targets = take(sizeof(float) * 4 * g.m);  // paired field layout (also holds a plain field)
     F.defect = take(precomputed_defect(g) ? sizeof(float) * 2 * g.m : 0);
     F.scratch = take(sizeof(float) * 64);
     const size_t nn = (size_t)(n > 0 ? n : 1);
@@ -93,22 +96,40 @@ static FullLayout full_layout(const Geo& g, int64_t n) {
 
 static bool k_ok(int k) { return k >= 0 && k <= INIM_MAX_K; }
 
-// One iteration.  `counts` must be zero on entry; `counts_next` (optional) is cleared
-// by the smoothing pass for the next iteration.
+// Chaining of consecutive iterations inside a run: the move of iteration t splats its
+// output into iteration t+1's count buffer and clears t+1's device scalars.
+struct Chain {
+    bool splatted;       // this iteration's counts were filled by the previous move
+    bool splat_next;     // fuse the next iteration's splat into this move
+    float *next_exc, *next_disp;
+};
+
+// One iteration.  `counts` must be zero on entry (or already filled, chain.splatted);
+// `counts_next` (optional) is cleared by the smoothing pass for the next iteration.
+// With `pairs` the field is (also) written in the paired layout and the move reads
+// that; `targets` may then be null.
 static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, const Geo& g, int kernel_size,
                              float background, const float* defect, uint32_t* counts, uint32_t* counts_next, float* d,
                              float* targets, float* max_exc, float* disp, float stop_eps, int* state, const Ws& ws,
-                             const CUtensorMap* map, cudaStream_t st) {
+                             const CUtensorMap* map, cudaStream_t st, float* pairs = nullptr,
+                             const Chain& chain = Chain{false, false, nullptr, nullptr}) {
     const int* flag = stop_eps > 0.f ? state : nullptr;
-    int rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp);
-    if (rc) return rc;
+    int rc = 0;
+    if (!chain.splatted) {
+        rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp);
+        if (rc) return rc;
+    }
     rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, ws, flag, st);
     if (rc) return rc;
-    rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st);
+    rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st, pairs);
     if (rc) return rc;
-    rc = launch_sample_f32(targets, g.k, pts_in, pts_out, n, 1, disp, flag, st);
+    uint32_t* sn = chain.splat_next ? counts_next : nullptr;
+    rc = pairs ? launch_sample_f32(pairs, g.k, pts_in, pts_out, n, 1, disp, flag, st, true, sn, chain.next_exc,
+                                   chain.next_disp)
+               : launch_sample_f32(targets, g.k, pts_in, pts_out, n, 1, disp, flag, st, false, sn, chain.next_exc,
+                                   chain.next_disp);
     if (rc) return rc;
     if (flag) {
         iter_end_kernel<<<1, 1, 0, st>>>(disp, stop_eps, state);
@@ -185,22 +206,35 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     // cell; off until its hot-cell atomics are privatised (it currently costs more than
     // the gathers it saves).
     constexpr bool kSortPoints = false;
-    if (key.n > 0) {
-        int rc = kSortPoints ? launch_sort_points(pts, key.n, g.k, hist, rank, sortA, perm, st)
-                             : (int)cudaMemcpyAsync(sortA, pts, pbytes, cudaMemcpyDeviceToDevice, st);
+    if (kSortPoints && key.n > 0) {
+        int rc = launch_sort_points(pts, key.n, g.k, hist, rank, sortA, perm, st);
         if (rc) return rc;
     }
-    float* bufs[2] = {sortA, sortB};
+    // Point buffers: the first move reads the caller's array and the last one writes it
+    // back (no staging copies); in between the moves ping-pong through sortA / sortB.
+    float* bufs[2] = {sortB, sortA};
+    auto pos_in = [&](int t) -> float* {
+        if (t == 0) return kSortPoints ? sortA : pts;
+        return bufs[t & 1];
+    };
+    auto pos_out = [&](int t) -> float* {
+        if (t == key.iters - 1 && !kSortPoints) return pts;
+        return bufs[(t + 1) & 1];
+    };
+    // per-iteration device scalars: recorded arrays, else two alternating scratch slots
+    // (the move of iteration t clears iteration t+1's slot while t's is still live)
+    auto disp_at = [&](int t) { return disp ? disp + t : scratch + 2 * (t & 1); };
+    auto exc_at = [&](int t) { return excursions ? excursions + t : scratch + 2 * (t & 1) + 1; };
     for (int t = 0; t < key.iters; ++t) {
-        float* src = bufs[t & 1];
-        float* dst = bufs[(t + 1) & 1];
-        float* tg = fields ? fields + (size_t)t * 2 * g.m : tg_scratch;
-        float* dsp = disp ? disp + t : scratch;
-        float* ex = excursions ? excursions + t : scratch + 1;
+        float* src = pos_in(t);
+        float* dst = pos_out(t);
+        float* tg = fields ? fields + (size_t)t * 2 * g.m : nullptr;  // plain field only when recorded
         uint32_t* cur = counts + (size_t)(t & 1) * g.m;
         uint32_t* next = counts + (size_t)((t + 1) & 1) * g.m;
-        int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, tg, ex, dsp, key.eps,
-                                   state, w, mp, st);
+        const bool more = t + 1 < key.iters && key.n > 0;
+        const Chain chain{t > 0, more, more ? exc_at(t + 1) : nullptr, more ? disp_at(t + 1) : nullptr};
+        int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, tg, exc_at(t),
+                                   disp_at(t), key.eps, state, w, mp, st, tg_scratch, chain);
         if (rc) return rc;
         if (frames && key.n > 0) {
             float* fr = frames + (size_t)(t + 1) * 2 * key.n;
@@ -209,9 +243,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
             if (rc) return rc;
         }
     }
-    if (key.n > 0)
-        return kSortPoints ? launch_unpermute(bufs[key.iters & 1], perm, key.n, pts, st)
-                           : (int)cudaMemcpyAsync(pts, bufs[key.iters & 1], pbytes, cudaMemcpyDeviceToDevice, st);
+    if (kSortPoints && key.n > 0 && key.iters > 0) return launch_unpermute(pos_out(key.iters - 1), perm, key.n, pts, st);
     return 0;
 }
 
@@ -535,11 +567,12 @@ int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, in
 }
 
 int inim_kernels_per_iteration(int k) {
-    // splat, smooth_h, smooth_v(+reduce), 4 carry-scan kernels, write_field, sample
-    // (+ iter_end when the displacement criterion is on).  Per run, not per iteration:
-    // one memset node and one flat-response kernel (grids <= 2048^2).
+    // smooth_h, smooth_v(+reduce), 3 carry-scan kernels (lines, chains, marg),
+    // write_field, move (+ iter_end when the displacement criterion is on).  The move
+    // of iteration t splats iteration t+1, so a run adds one splat kernel and one memset
+    // node in total.
     (void)k;
-    return 9;
+    return 7;
 }
 
 }  // extern "C"

@@ -37,22 +37,21 @@ inline Geo make_geo(int k) {
 // Byte offsets into the caller-provided workspace (all 256-byte aligned).
 struct WsLayout {
     size_t tmp;      // float [s*s]            horizontal smoothing pass
-    size_t colsum;   // float [B][s]           per-band column sums
+    size_t inpre;    // float [B][s]           in-tile inclusive row prefix of the band's column sums
+    size_t tiletot;  // double [B][NX]         tile totals
     size_t rowsum;   // float [s][NX]          per-tile row sums
     size_t ulbot;    // float [B][s]           in-tile up-left chain of V at the band's last row
     size_t urbot;    // float [B][s]           in-tile up-right chain of V at the band's last row
     size_t ule;      // float [B][NX][TH]      up-left chain at each tile's last column
     size_t ure;      // float [B][NX][TH]      up-right chain at each tile's first column
-    size_t batl;     // double [B][s]          inclusive row prefix of colsum per band
-    size_t ulb2;     // double [B][s]          completed up-left bottom chains
-    size_t urb2;     // double [B][s]          completed up-right bottom chains
+    size_t tilepre;  // double [B][NX]         exclusive prefix over tiles of the tile totals
+    size_t btot;     // double [B]             band totals
+    size_t bandpre;  // double [B+1]           exclusive prefix of the band totals (TLcar_b[s-1])
     size_t tlcar;    // double [B+1][s]        rect_tl at the row above each band (row s-1 for b=B)
-    size_t x1;       // double [B][s]          ULcar - TLcar
-    size_t x2;       // double [B][s+TH]       URcar + TLcar[c-1], extended with TLcar[s-1]
-    size_t ulrow;    // double [s]             up-left chain of U along the last row (UL[s-1][c])
-    size_t urrow;    // double [s]             up-right chain of U along the last row (UR[s-1][c])
+    size_t x1;       // double [B+1][s]        ULcar - TLcar (row B: along the last row)
+    size_t x2;       // double [B+1][s+TH]     URcar + TLcar[c-1], extended with TLcar[s-1]
     size_t hc;       // double [s][NX]         row prefix of d up to each tile's first column
-    size_t rpre;     // double [s]             row totals, then their prefix
+    size_t rpre;     // double [s]             in-band row prefix, then Rpre
     size_t apre;     // double [2s-1]          prefix of anti-diagonal totals
     size_t dsuf;     // double [2s-1]          suffix of diagonal totals
     size_t total;    // double [1]
@@ -72,20 +71,19 @@ inline WsLayout make_layout(const Geo& g) {
     };
     const size_t s = g.s, B = g.B, NX = g.NX, TH = g.TH;
     L.tmp = take(sizeof(float) * s * s);
-    L.colsum = take(sizeof(float) * B * s);
+    L.inpre = take(sizeof(float) * B * s);
+    L.tiletot = take(sizeof(double) * B * NX);
     L.rowsum = take(sizeof(float) * s * NX);
     L.ulbot = take(sizeof(float) * B * s);
     L.urbot = take(sizeof(float) * B * s);
     L.ule = take(sizeof(float) * B * NX * TH);
     L.ure = take(sizeof(float) * B * NX * TH);
-    L.batl = take(sizeof(double) * B * s);
-    L.ulb2 = take(sizeof(double) * B * s);
-    L.urb2 = take(sizeof(double) * B * s);
+    L.tilepre = take(sizeof(double) * B * NX);
+    L.btot = take(sizeof(double) * B);
+    L.bandpre = take(sizeof(double) * (B + 1));
     L.tlcar = take(sizeof(double) * (B + 1) * s);
-    L.x1 = take(sizeof(double) * B * s);
-    L.x2 = take(sizeof(double) * B * (s + TH));
-    L.ulrow = take(sizeof(double) * s);
-    L.urrow = take(sizeof(double) * s);
+    L.x1 = take(sizeof(double) * (B + 1) * s);
+    L.x2 = take(sizeof(double) * (B + 1) * (s + TH));
     L.hc = take(sizeof(double) * s * NX);
     L.rpre = take(sizeof(double) * s);
     L.apre = take(sizeof(double) * (2 * s - 1));
@@ -99,20 +97,19 @@ inline WsLayout make_layout(const Geo& g) {
 // Typed view of the workspace, passed by value to kernels.
 struct Ws {
     float* tmp;
-    float* colsum;
+    float* inpre;
+    double* tiletot;
     float* rowsum;
     float* ulbot;
     float* urbot;
     float* ule;
     float* ure;
-    double* batl;
-    double* ulb2;
-    double* urb2;
+    double* tilepre;
+    double* btot;
+    double* bandpre;
     double* tlcar;
     double* x1;
     double* x2;
-    double* ulrow;
-    double* urrow;
     double* hc;
     double* rpre;
     double* apre;
@@ -125,20 +122,19 @@ inline Ws make_ws(void* base, const WsLayout& L) {
     char* b = static_cast<char*>(base);
     Ws w;
     w.tmp = reinterpret_cast<float*>(b + L.tmp);
-    w.colsum = reinterpret_cast<float*>(b + L.colsum);
+    w.inpre = reinterpret_cast<float*>(b + L.inpre);
+    w.tiletot = reinterpret_cast<double*>(b + L.tiletot);
     w.rowsum = reinterpret_cast<float*>(b + L.rowsum);
     w.ulbot = reinterpret_cast<float*>(b + L.ulbot);
     w.urbot = reinterpret_cast<float*>(b + L.urbot);
     w.ule = reinterpret_cast<float*>(b + L.ule);
     w.ure = reinterpret_cast<float*>(b + L.ure);
-    w.batl = reinterpret_cast<double*>(b + L.batl);
-    w.ulb2 = reinterpret_cast<double*>(b + L.ulb2);
-    w.urb2 = reinterpret_cast<double*>(b + L.urb2);
+    w.tilepre = reinterpret_cast<double*>(b + L.tilepre);
+    w.btot = reinterpret_cast<double*>(b + L.btot);
+    w.bandpre = reinterpret_cast<double*>(b + L.bandpre);
     w.tlcar = reinterpret_cast<double*>(b + L.tlcar);
     w.x1 = reinterpret_cast<double*>(b + L.x1);
     w.x2 = reinterpret_cast<double*>(b + L.x2);
-    w.ulrow = reinterpret_cast<double*>(b + L.ulrow);
-    w.urrow = reinterpret_cast<double*>(b + L.urrow);
     w.hc = reinterpret_cast<double*>(b + L.hc);
     w.rpre = reinterpret_cast<double*>(b + L.rpre);
     w.apre = reinterpret_cast<double*>(b + L.apre);
@@ -171,8 +167,10 @@ int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const 
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st);
 int launch_write_tables(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, float* tables8,
                         cudaStream_t st);
+// targets: standard (s, s, 2) field or null; pairs: paired (s, s, 4) layout for the
+// move kernel or null.
 int launch_write_field(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const float* defect,
-                       float* targets, float* max_exc, const int* state, cudaStream_t st);
+                       float* targets, float* max_exc, const int* state, cudaStream_t st, float* pairs = nullptr);
 int make_tensor_map_2d(CUtensorMap* map, const float* base, int s, int box_w, int box_h);
 
 }  // namespace inim

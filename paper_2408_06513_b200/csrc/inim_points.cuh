@@ -37,6 +37,26 @@ __device__ __forceinline__ void bilinear(const float2* __restrict__ tg, int s, T
     oy = w00 * (T)t00.y + w10 * (T)t10.y + w01 * (T)t01.y + w11 * (T)t11.y;
 }
 
+// The same blend from the paired field layout (slot i of row j = (t(i, j), t(i + 1, j)),
+// see WriteOut::pairs): two 16-byte loads instead of four 8-byte ones, identical values
+// and arithmetic.
+__device__ __forceinline__ void bilinear_pairs(const float4* __restrict__ tp, int s, float x, float y, float& ox,
+                                               float& oy) {
+    const float sx = x * (float)s, sy = y * (float)s;
+    int i0 = (int)floorf(sx), j0 = (int)floorf(sy);
+    i0 = i0 < 0 ? 0 : (i0 > s - 2 ? s - 2 : i0);
+    j0 = j0 < 0 ? 0 : (j0 > s - 2 ? s - 2 : j0);
+    const float fx = sx - (float)i0, fy = sy - (float)j0;
+    const float w00 = (1.f - fx) * (1.f - fy);
+    const float w10 = fx * (1.f - fy);
+    const float w01 = (1.f - fx) * fy;
+    const float w11 = fx * fy;
+    const int64_t base = (int64_t)j0 * s + i0;
+    const float4 r0 = __ldg(tp + base), r1 = __ldg(tp + base + s);
+    ox = w00 * r0.x + w10 * r0.z + w01 * r1.x + w11 * r1.z;
+    oy = w00 * r0.y + w10 * r0.w + w01 * r1.y + w11 * r1.w;
+}
+
 template <typename T>
 __device__ __forceinline__ T clip01(T v) {
     return v < (T)0 ? (T)0 : (v > (T)1 ? (T)1 : v);

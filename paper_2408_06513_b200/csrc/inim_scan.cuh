@@ -1,28 +1,38 @@
 // Carry scan (phase 2 of the integral pass) as per-item device functions, shared by
 // the standalone scan launches (scan.cu) and the persistent iteration kernel (mega.cu).
 // Every function is called by a whole CTA (blockDim a multiple of 32, <= 1024) for one
-// work item and contains CTA-wide barriers.
+// work item and may contain CTA-wide barriers.
 //
-//   band_rows  item = band b: inclusive row prefix of the column sums (BATL) and
-//              completion of the band-bottom chains with the neighbouring tiles' edges
-//   colscan    item < ceil(s/32): TLcar_b[c] = sum_{b'<b} BATL[b'][c] for 32 columns
-//              (32 columns x NY band chunks, chunk sums scanned in shared memory);
-//              item >= ceil(s/32): NY rows each (one warp per row): HC and row totals
-//   diagscan   the diagonal recurrences as prefix sums along sheared columns:
-//                ULcar_{b+1}[c] = G_b[c] + ULcar_b[c-TH],  G_b[c] = ULbot_b[c] + TLcar_b[c] - TLcar_b[c-TH]
-//                URcar_{b+1}[c] = H_b[c] + URcar_b[c+TH],  H_b[c] = URbot_b[c] + TLcar_b[min(c+TH-1,s-1)] - TLcar_b[c-1]
-//              stored as X1 = ULcar - TLcar, X2 = URcar + TLcar[c-1] (+ border), and the
-//              virtual band b = B gives the chains along the last row (ULrow, URrow)
-//   marg       Rpre per band (TLcar_b[s-1] + in-band prefix of the row totals),
-//              C = TLcar_B[s-1], and the diagonal marginals read off the chains:
-//                Dsuf[d>=0] = UL[s-1-d][s-1],  Dsuf[d<0] = UL[s-1][s-1+d] + C - Cpre[s-1+d]
-//                Apre[q<s]  = UR[q][0],        Apre[q>=s] = UR[s-1][q-s+1] + Cpre[q-s]
-// Every sum has a fixed order (deterministic).
+//   lines   item = band b: for each row j of the band the exclusive prefix over tiles
+//           of the row sums (HC[j][x]) and the in-band prefix of the row totals; for the
+//           band the exclusive prefix over tiles of the tile totals (tilepre) and the
+//           band total.
+//   chains  item = 32 consecutive chains of one kind x NY band chunks.  With the
+//           band-local row prefix of the column sums  batl_b[c] = tilepre_b[c/TW] +
+//           inpre_b[c]  every carry is a plain scan over the bands of band-local terms:
+//             TL: TLcar_{b+1}[c] = TLcar_b[c] + batl_b[c]
+//             X1: X1_{b+1}[c]    = X1_b[c-TH] + ULbot2_b[c] - batl_b[c]
+//             X2: X2_{b+1}[c]    = X2_b[c+TH] + URbot2_b[c] + batl_b[c-1],
+//                 X2_b[c >= s]   = TLcar_b[s-1]  (injected where a chain enters the grid)
+//           where X1 = ULcar - TLcar and X2 = URcar + TLcar[c-1] are the write pass's
+//           diagonal carries and ULbot2 / URbot2 complete the band-bottom chains with
+//           the neighbouring tiles' edge chains.  Substituting TLcar_{b+1} = TLcar_b +
+//           batl_b into the ULcar / URcar recurrences gives the X1 / X2 forms, so the
+//           three scans are independent of each other.
+//   marg    Rpre (TLcar_b[s-1] + in-band prefix), C, and the diagonal marginals:
+//             Dsuf[d>=0] = ULE + TLcar_b[s-1] + X1_b[s-2-r]   (row j = s-1-d = bTH + r)
+//             Dsuf[d<0]  = X1_B[s-1+d] + C
+//             Apre[q<s]  = URE + X2_b[r+1]                     (row q = bTH + r)
+//             Apre[q>=s] = X2_B[q-s+1]
+// tests/tile_model.py restates the algebra in numpy against the oracle.  Every sum has
+// a fixed order (deterministic).
 #pragma once
 
 #include "inim_internal.cuh"
 
 namespace inim {
+
+constexpr int kMaxBands = 512;  // s / TH for s = 16384, TH = 32
 
 // Block-wide exclusive scan of one double per thread.  *total receives the block total.
 __device__ __forceinline__ double block_excl_scan(double v, double* sh /* 33 */, double* total) {
@@ -43,202 +53,191 @@ __device__ __forceinline__ double block_excl_scan(double v, double* sh /* 33 */,
     return r;
 }
 
-// Inclusive prefix of a row of n elements into dst, 4 elements per thread per tile.
+// Exclusive prefix of a line of n values (one warp, float64); returns the line total.
 template <typename T>
-__device__ __forceinline__ void row_prefix(const T* __restrict__ src, double* __restrict__ dst, int n, double* sh) {
-    constexpr int per = 4;
+__device__ __forceinline__ double warp_line_prefix(const T* __restrict__ src, double* __restrict__ dst, int n,
+                                                   int lane) {
     double carry = 0.0;
-    for (int base = 0; base < n; base += per * blockDim.x) {
-        const int i0 = base + per * threadIdx.x;
-        double v[per];
-        double loc = 0.0;
-#pragma unroll
-        for (int e = 0; e < per; ++e) {
-            v[e] = i0 + e < n ? (double)src[i0 + e] : 0.0;
-            loc += v[e];
+    for (int base = 0; base < n; base += 32) {
+        const int x = base + lane;
+        const double v = x < n ? (double)src[x] : 0.0;
+        const double inc = warp_inclusive_scan_d(v, lane);
+        if (x < n) dst[x] = carry + inc - v;
+        carry += __shfl_sync(kFull, inc, 31);
+    }
+    return carry;
+}
+
+__device__ __forceinline__ void lines_item(const Geo& g, const Ws& ws, int b, double* sh /* 33 */) {
+    const int TH = g.TH, NX = g.NX;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int a = b * TH;
+    for (int q = w; q <= TH; q += nw) {
+        if (q < TH) {
+            const int64_t j = a + q;
+            const double tot = warp_line_prefix(ws.rowsum + j * NX, ws.hc + j * NX, NX, lane);
+            if (lane == 0) sh[q] = tot;
+        } else {
+            const double tot =
+                warp_line_prefix(ws.tiletot + (int64_t)b * NX, ws.tilepre + (int64_t)b * NX, NX, lane);
+            if (lane == 0) ws.btot[b] = tot;
         }
+    }
+    __syncthreads();
+    if (w == 0) {
+        const double v = lane < TH ? sh[lane] : 0.0;
+        const double inc = warp_inclusive_scan_d(v, lane);
+        if (lane < TH) ws.rpre[a + lane] = inc;  // in-band prefix; marg adds TLcar_b[s-1]
+    }
+    __syncthreads();
+}
+
+// Exclusive prefix of the band totals into shared memory bp[0..B] (whole CTA).
+__device__ __forceinline__ void band_prefix(const Geo& g, const Ws& ws, double* bp, double* sh /* 33 */) {
+    const int B = g.B;
+    double carry = 0.0;
+    for (int base = 0; base < B; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        const double v = q < B ? ws.btot[q] : 0.0;
         double tot;
-        const double off = block_excl_scan(loc, sh, &tot);
-        double run = carry + off;
-#pragma unroll
-        for (int e = 0; e < per; ++e) {
-            run += v[e];
-            if (i0 + e < n) dst[i0 + e] = run;
-        }
+        const double ex = block_excl_scan(v, sh, &tot);
+        if (q < B) bp[q] = carry + ex;
         carry += tot;
     }
+    if (threadIdx.x == 0) bp[B] = carry;
+    __syncthreads();
 }
 
-__device__ __forceinline__ void band_rows_item(const Geo& g, const Ws& ws, int b, double* sh) {
-    const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX;
-    row_prefix<float>(ws.colsum + (int64_t)b * s, ws.batl + (int64_t)b * s, s, sh);
-    const float* __restrict__ ulbot = ws.ulbot + (int64_t)b * s;
-    const float* __restrict__ urbot = ws.urbot + (int64_t)b * s;
-    const float* __restrict__ ule = ws.ule + (int64_t)b * NX * TH;
-    const float* __restrict__ ure = ws.ure + (int64_t)b * NX * TH;
-    for (int c = threadIdx.x; c < s; c += blockDim.x) {
-        const int x = c / TW, u = c - x * TW;
-        double ul = ulbot[c];
-        const int rr = TH - 2 - u;  // row where the chain leaves the tile on the left
-        if (x > 0 && rr >= 0) ul += ule[(x - 1) * TH + rr];
-        double ur = urbot[c];
-        const int rq = TH - 1 - (TW - u);
-        if (x < NX - 1 && rq >= 0) ur += ure[(x + 1) * TH + rq];
-        ws.ulb2[(int64_t)b * s + c] = ul;
-        ws.urb2[(int64_t)b * s + c] = ur;
+__host__ __device__ inline int chain_groups_tl(const Geo& g) { return (g.s + 31) / 32; }
+__host__ __device__ inline int chain_groups_x(const Geo& g) { return (g.s + g.B * g.TH + 31) / 32; }
+__host__ __device__ inline int chains_items(const Geo& g) { return chain_groups_tl(g) + 2 * chain_groups_x(g); }
+__host__ __device__ inline int chain_kind(const Geo& g, int item) {
+    const int ntl = chain_groups_tl(g);
+    return item < ntl ? 0 : (item < ntl + chain_groups_x(g) ? 1 : 2);
+}
+// band chunks per chain (warps per CTA): short serial chunks on small grids
+__host__ __device__ inline int chain_warps(const Geo& g) {
+    const int ny = g.B / 4;
+    return ny < 1 ? 1 : (ny > 16 ? 16 : ny);
+}
+
+template <int KIND>
+struct ChainTerms {
+    const Geo& g;
+    const Ws& ws;
+    const double* bp;
+    int kk;
+    __device__ __forceinline__ int col(int b) const {
+        return KIND == 0 ? kk : (KIND == 1 ? kk - (g.B - b) * g.TH : kk - b * g.TH);
     }
-}
-
-// Exclusive prefix over the NY chunk rows of part[ty][tx], per column tx.
-__device__ __forceinline__ double chunk_exclusive(double (*part)[33], int tx, int ty) {
-    double off = 0.0;
-    for (int q = 0; q < ty; ++q) off += part[q][tx];
-    return off;
-}
-
-__host__ __device__ inline int colscan_items(const Geo& g, int ny) { return (g.s + 31) / 32 + (g.s + ny - 1) / ny; }
-
-__device__ __forceinline__ void colscan_item(const Geo& g, const Ws& ws, int item, double (*part)[33]) {
-    const int s = g.s, B = g.B, NX = g.NX;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, NY = blockDim.x >> 5;
-    const int ncb = (s + 31) / 32;
-    if (item < ncb) {
-        const int c = item * 32 + tx;
-        const int CH = (B + NY - 1) / NY;
-        const int b0 = ty * CH, b1 = min(B, b0 + CH);
-        const double* __restrict__ batl = ws.batl;
-        double loc = 0.0;
-        if (c < s)
-            for (int b = b0; b < b1; ++b) loc += batl[(int64_t)b * s + c];
-        part[ty][tx] = loc;
-        __syncthreads();
-        double run = chunk_exclusive(part, tx, ty);
-        if (c < s) {
-            double* __restrict__ tl = ws.tlcar;
-            for (int b = b0; b < b1; ++b) {
-                tl[(int64_t)b * s + c] = run;
-                run += batl[(int64_t)b * s + c];
-            }
-            if (b1 == B && b0 < b1) tl[(int64_t)B * s + c] = run;
-        }
-        __syncthreads();
-        return;
+    __device__ __forceinline__ double batl(int b, int c) const {
+        return ws.tilepre[(int64_t)b * g.NX + c / g.TW] + (double)ws.inpre[(int64_t)b * g.s + c];
     }
-    // rows: HC[j][x] = exclusive prefix over x of rowsum[j][x]; row total -> rpre[j]
-    const int j = (item - ncb) * NY + ty;
-    if (j < s) {
-        const float* __restrict__ rs = ws.rowsum + (int64_t)j * NX;
-        double* __restrict__ hc = ws.hc + (int64_t)j * NX;
-        double carry = 0.0;
-        for (int base = 0; base < NX; base += 32) {
-            const int x = base + tx;
-            const double v = x < NX ? (double)rs[x] : 0.0;
-            const double inc = warp_inclusive_scan_d(v, tx);
-            if (x < NX) hc[x] = carry + inc - v;
-            carry += __shfl_sync(kFull, inc, 31);
-        }
-        if (tx == 0) ws.rpre[j] = carry;
-    }
-}
-
-// items: [0, 2*nchunk) chain groups (UL then UR), then ceil(B*TH/blockDim) border items.
-__host__ __device__ inline int diagscan_items(const Geo& g, int nthreads) {
-    const int nk = g.s + g.B * g.TH;
-    return 2 * ((nk + 31) / 32) + (g.B * g.TH + nthreads - 1) / nthreads;
-}
-
-__device__ __forceinline__ void diagscan_item(const Geo& g, const Ws& ws, int item, double (*part)[33]) {
-    const int s = g.s, B = g.B, TH = g.TH;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, NY = blockDim.x >> 5;
-    const double* __restrict__ TLc = ws.tlcar;
-    auto TL = [&](int b, int c) -> double { return c >= 0 ? TLc[(int64_t)b * s + c] : 0.0; };
-    const int nk = s + B * TH;
-    const int ngroups = (nk + 31) / 32;
-    if (item >= 2 * ngroups) {  // X2 beyond the right border: TLcar_b[s-1]
-        const int q = (item - 2 * ngroups) * blockDim.x + threadIdx.x;
-        if (q < B * TH) {
-            const int b = q / TH, e = q % TH;
-            ws.x2[(int64_t)b * (s + TH) + s + e] = TL(b, s - 1);
-        }
-        return;
-    }
-    const bool up_left = item < ngroups;
-    const int kk = (up_left ? item : item - ngroups) * 32 + tx;  // chain index
-    const int CH = (B + NY - 1) / NY;
-    const int b0 = ty * CH, b1 = min(B, b0 + CH);
-    // UL: kappa = kk - B*TH in [-B*TH, s); step term G_b[kappa + (b+1) TH]
-    // UR: kappa = kk in [0, s + B*TH);       step term H_b[kappa - (b+1) TH]
-    const int kappa = up_left ? kk - B * TH : kk;
-    auto term = [&](int b) -> double {
-        if (kk >= nk) return 0.0;
-        if (up_left) {
-            const int c = kappa + (b + 1) * TH;
-            if (c < 0 || c >= s) return 0.0;
-            return ws.ulb2[(int64_t)b * s + c] + TL(b, c) - TL(b, c - TH);
-        }
-        const int c = kappa - (b + 1) * TH;
+    // step b -> b + 1
+    __device__ __forceinline__ double term(int b) const {
+        const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX;
+        if (KIND == 0) return batl(b, kk);
+        const int c = col(b + 1);
         if (c < 0 || c >= s) return 0.0;
-        return ws.urb2[(int64_t)b * s + c] + TL(b, min(c + TH - 1, s - 1)) - TL(b, c - 1);
-    };
+        const int x = c / TW, u = c - x * TW;
+        if (KIND == 1) {
+            double v = (double)ws.ulbot[(int64_t)b * s + c] - batl(b, c);
+            const int rr = TH - 2 - u;  // row where the chain leaves the tile on the left
+            if (x > 0 && rr >= 0) v += (double)ws.ule[((int64_t)b * NX + x - 1) * TH + rr];
+            return v;
+        }
+        double v = (double)ws.urbot[(int64_t)b * s + c] + (c > 0 ? batl(b, c - 1) : 0.0);
+        const int rq = TH - 1 - (TW - u);
+        if (x < NX - 1 && rq >= 0) v += (double)ws.ure[((int64_t)b * NX + x + 1) * TH + rq];
+        if (c + TH >= s) v += bp[b];  // the chain enters the grid: X2_b beyond the border
+        return v;
+    }
+    __device__ __forceinline__ void emit(int b, double run) const {
+        const int s = g.s, TH = g.TH;
+        const int c = col(b);
+        if (KIND == 0) {
+            ws.tlcar[(int64_t)b * s + c] = run;
+        } else if (KIND == 1) {
+            if (c >= 0 && c < s) ws.x1[(int64_t)b * s + c] = run;
+        } else {
+            if (c >= 0 && c < s) ws.x2[(int64_t)b * (s + TH) + c] = run;
+            else if (c >= s && c < s + TH) ws.x2[(int64_t)b * (s + TH) + c] = bp[b];
+        }
+    }
+};
+
+template <int KIND>
+__device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, double (*part)[33], const double* bp) {
+    const int B = g.B;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, NY = blockDim.x >> 5;
+    const bool live = kk < (KIND == 0 ? g.s : g.s + B * g.TH);
+    const int CH = (B + NY - 1) / NY;
+    const int b0 = min(B, ty * CH), b1 = min(B, b0 + CH);
+    const ChainTerms<KIND> T{g, ws, bp, kk};
+    constexpr int U = 4;  // terms in flight per thread
     double loc = 0.0;
-    for (int b = b0; b < b1; ++b) loc += term(b);
+    if (live) {
+        int b = b0;
+        for (; b + U <= b1; b += U) {
+            double t[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) t[q] = T.term(b + q);
+#pragma unroll
+            for (int q = 0; q < U; ++q) loc += t[q];
+        }
+        for (; b < b1; ++b) loc += T.term(b);
+    }
     part[ty][tx] = loc;
     __syncthreads();
-    double run = chunk_exclusive(part, tx, ty);  // chain value at band b0
-    __syncthreads();
-    if (kk >= nk) return;
-    const int bend = (b1 == B) ? B + 1 : b1;  // the last chunk also emits the virtual band B
-    for (int b = b0; b < bend; ++b) {
-        const int c = up_left ? kappa + b * TH : kappa - b * TH;
-        if (c >= 0 && c < s) {
-            if (b < B) {
-                if (up_left) ws.x1[(int64_t)b * s + c] = run - TL(b, c);
-                else ws.x2[(int64_t)b * (s + TH) + c] = run + TL(b, c - 1);
-            } else {
-                if (up_left) ws.ulrow[c] = run;
-                else ws.urrow[c] = run;
-            }
+    double run = 0.0;
+    for (int q = 0; q < ty; ++q) run += part[q][tx];
+    __syncthreads();  // `part` is reused by the caller's next item
+    if (!live) return;
+    int b = b0;
+    for (; b + U <= b1; b += U) {
+        double t[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) t[q] = T.term(b + q);
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            T.emit(b + q, run);
+            run += t[q];
         }
-        if (b < B) run += term(b);
     }
+    for (; b < b1; ++b) {
+        T.emit(b, run);
+        run += T.term(b);
+    }
+    if (b1 == B && b0 < b1) T.emit(B, run);  // the last chunk emits band B too
 }
 
-// items: ceil(B / NY) band groups (one warp per band: Rpre), then the 2s-1 marginal
-// entries in chunks of blockDim.
-__host__ __device__ inline int marg_items(const Geo& g, int nthreads) {
-    const int ny = nthreads / 32;
-    return (g.B + ny - 1) / ny + (2 * g.s - 1 + nthreads - 1) / nthreads;
+// bp: the band prefix (band_prefix) for X2 items, else unused.
+__device__ __forceinline__ void chains_item(const Geo& g, const Ws& ws, int item, double (*part)[33],
+                                            const double* bp) {
+    const int tx = threadIdx.x & 31;
+    const int ntl = chain_groups_tl(g), nxg = chain_groups_x(g);
+    if (item < ntl) chains_body<0>(g, ws, item * 32 + tx, part, bp);
+    else if (item < ntl + nxg) chains_body<1>(g, ws, (item - ntl) * 32 + tx, part, bp);
+    else chains_body<2>(g, ws, (item - ntl - nxg) * 32 + tx, part, bp);
 }
 
-__device__ __forceinline__ void marg_item(const Geo& g, const Ws& ws, int item) {
+__host__ __device__ inline int marg_entries(const Geo& g) { return 2 * g.s - 1; }
+
+// One entry q of the marginals (q < 2s - 1); bandpre must be complete.
+__device__ __forceinline__ void marg_entry(const Geo& g, const Ws& ws, int q) {
     const int s = g.s, TH = g.TH, NX = g.NX, B = g.B;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, NY = blockDim.x >> 5;
-    const int nbg = (B + NY - 1) / NY;
-    const double* __restrict__ cpre = ws.tlcar + (int64_t)B * s;
-    const double C = cpre[s - 1];
-    if (item < nbg) {
-        const int b = item * NY + w;
-        if (b < B) {
-            const int a = b * TH;
-            const double tot = lane < TH ? ws.rpre[a + lane] : 0.0;  // row totals (colscan)
-            const double inc = warp_inclusive_scan_d(tot, lane);
-            __syncwarp();
-            if (lane < TH) ws.rpre[a + lane] = ws.tlcar[(int64_t)b * s + s - 1] + inc;
-        }
-        if (item == 0 && threadIdx.x == 0) *ws.total = C;
-        return;
-    }
-    const int q = (item - nbg) * blockDim.x + threadIdx.x;
-    if (q >= 2 * s - 1) return;
+    const double* __restrict__ bandpre = ws.bandpre;
+    const double C = bandpre[B];
+    if (q == 0) *ws.total = C;
+    if (q < s) ws.rpre[q] += bandpre[q / TH];  // in-band prefix -> Rpre
     const int delta = q - (s - 1);
     double dv;
     if (delta >= 0) {
         const int j = s - 1 - delta, b = j / TH, r = j - b * TH, c2 = s - 2 - r;
-        dv = (double)ws.ule[((int64_t)b * NX + NX - 1) * TH + r] + ws.tlcar[(int64_t)b * s + s - 1] +
+        dv = (double)ws.ule[((int64_t)b * NX + NX - 1) * TH + r] + bandpre[b] +
              (c2 >= 0 ? ws.x1[(int64_t)b * s + c2] : 0.0);
     } else {
-        const int c = s - 1 + delta;
-        dv = ws.ulrow[c] + C - cpre[c];
+        dv = ws.x1[(int64_t)B * s + s - 1 + delta] + C;
     }
     ws.dsuf[q] = dv;
     double av;
@@ -246,8 +245,7 @@ __device__ __forceinline__ void marg_item(const Geo& g, const Ws& ws, int item) 
         const int b = q / TH, r = q - b * TH;
         av = (double)ws.ure[(int64_t)b * NX * TH + r] + ws.x2[(int64_t)b * (s + TH) + r + 1];
     } else {
-        const int i = q - (s - 1);
-        av = ws.urrow[i] + cpre[i - 1];
+        av = ws.x2[(int64_t)B * (s + TH) + q - (s - 1)];
     }
     ws.apre[q] = av;
 }

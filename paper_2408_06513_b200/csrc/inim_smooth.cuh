@@ -4,6 +4,7 @@
 // CTA-wide barriers, so every thread of the CTA must call it.
 #pragma once
 
+#include "inim_taps.cuh"
 #include "inim_tiles.cuh"
 
 namespace inim {
@@ -14,7 +15,8 @@ struct Taps {
     float w[2 * kMaxR + 1];
 };
 
-// out[p] = sum_{t=0}^{2R} w[t] * line(p + t),  p in [0, n).  Register-blocked: P partial
+// out[p] = sum_{t=0}^{2R} w[t] * line(p + t),  p in [0, n), w = TapsOf<R / 3> (the taps are
+// compile-time immediates of FFMA; `taps` is unused).  Register-blocked: P partial
 // outputs per thread, every input read once per P outputs; taps are constant-bank
 // operands of FFMA.
 template <int R, int P, typename Load, typename Store>
@@ -31,7 +33,7 @@ __device__ __forceinline__ void fir_line(const Taps& taps, int n, Load line, Sto
 #pragma unroll
             for (int pp = 0; pp < P; ++pp) {
                 const int t = q - pp;
-                if (t >= 0 && t < NT) acc[pp] = fmaf(taps.w[t], v, acc[pp]);
+                if (t >= 0 && t < NT) acc[pp] = fmaf(TapsOf<R / 3>::w(t), v, acc[pp]);
             }
         }
 #pragma unroll
@@ -40,7 +42,7 @@ __device__ __forceinline__ void fir_line(const Taps& taps, int n, Load line, Sto
     for (; p0 < n; ++p0) {
         float acc = 0.f;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) acc = fmaf(taps.w[t], line(p0 + t), acc);
+        for (int t = 0; t < NT; ++t) acc = fmaf(TapsOf<R / 3>::w(t), line(p0 + t), acc);
         store(p0, acc);
     }
 }

@@ -40,7 +40,8 @@ INIM_DEV void store_row_cs(float* p, const float (&v)[CPL]) {
 
 // ------------------------------------------------------------------ phase 1: reduce
 // src: tile origin (shared or global), row stride ld.  Writes the per-tile aggregates:
-//   colsum[b][c], ulbot[b][c], urbot[b][c] (in-tile chains of the column prefix V at the
+//   inpre[b][c] (in-tile row prefix of the column sums), tiletot[b][x], ulbot[b][c],
+//   urbot[b][c] (in-tile chains of the column prefix V at the
 //   band's last row), ule/ure[b][x][r] (chains at the tile's last / first column, complete
 //   in-band values since TW >= TH), rowsum[j][x].
 template <int CPL>
@@ -88,17 +89,26 @@ __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const
     }
     const int a = b * TH, i0 = x * TW;
     const int64_t tile = (int64_t)b * NX + x;
+    // in-tile inclusive row prefix of the column sums (float64 scan over the lanes) and
+    // the tile total
+    double lsum = 0.0;
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) lsum += (double)V[e];
+    const double linc = warp_inclusive_scan_d(lsum, lane);
     if (act) {
-        float* cs = ws.colsum + (int64_t)b * s + i0 + u0;
+        float* ip = ws.inpre + (int64_t)b * s + i0 + u0;
         float* ub = ws.ulbot + (int64_t)b * s + i0 + u0;
         float* rb = ws.urbot + (int64_t)b * s + i0 + u0;
+        double run = linc - lsum;
 #pragma unroll
         for (int e = 0; e < CPL; ++e) {
-            cs[e] = V[e];
+            run += (double)V[e];
+            ip[e] = (float)run;
             ub[e] = UL[e];
             rb[e] = UR[e];
         }
     }
+    if (lane == 31) ws.tiletot[tile] = linc;
     if (lane < TH) {
         ws.ule[tile * TH + lane] = ule_mine;
         ws.ure[tile * TH + lane] = ure_mine;
@@ -139,9 +149,10 @@ __device__ __forceinline__ double2 flat_response_at(int i, int j, int k) {
 // ------------------------------------------------------------------- phase 3: write
 struct WriteOut {
     float* tables8;       // MODE 0
-    float* targets;       // MODE 1: (s, s, 2)
-    const float* defect;  // MODE 1: (s, s, 2) or null (closed form)
-    float* max_exc;       // MODE 1
+    float* targets;       // MODE 1/2: (s, s, 2), or null
+    const float* defect;  // MODE 2: (s, s, 2)
+    float* max_exc;       // MODE 1/2
+    float* pairs;         // MODE 1/2: (s, s, 4) = (t(i, j), t(i + 1, j)), or null
 };
 
 // Sliding window over a per-band vector indexed by (column +/- row): lane l holds the
@@ -168,15 +179,51 @@ INIM_DEV void slide_right(T (&w)[CPL], T ext, int r, int lane, int last) {  // i
     w[CPL - 1] = in;
 }
 
+// Region pixel counts of a constant s x s texture (exact; int32 is enough for k <= 14).
+// wedge_up count: (j + 1) + g(min(j, i)) + g(min(j, s - 1 - i)),  g(L) = L (2j + 1 - L) / 2
+// (each L (2j + 1 - L) is even).  ri = s - 1 - i, tj1 = 2j + 1.
+INIM_DEV int flat_up_count(int i, int ri, int j, int tj1) {
+    const int l1 = min(j, i), l2 = min(j, ri);
+    return (j + 1) + ((l1 * (tj1 - l1) + l2 * (tj1 - l2)) >> 1);
+}
+INIM_DEV int64_t flat_apre_count(int sg, int s) {  // #{i' + j' <= sg}
+    const int64_t S = s;
+    return sg <= s - 1 ? (int64_t)(sg + 1) * (sg + 2) / 2 : S * S - (2 * S - 2 - sg) * (2 * S - 1 - sg) / 2;
+}
+INIM_DEV int64_t flat_dsuf_count(int dl, int s) {  // #{i' - j' >= dl}
+    const int64_t S = s;
+    return dl >= 0 ? (S - dl) * (S - dl + 1) / 2 : S * S - (S + dl - 1) * (S + dl) / 2;
+}
+
+template <int CPL>
+INIM_DEV void load_row_g(const float* __restrict__ p, float (&v)[CPL]) {
+    if constexpr (CPL == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else if constexpr (CPL == 2) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    } else {
+        v[0] = __ldg(p);
+    }
+}
+
 // MODE 0: stream the eight tables (float32 assembly from float64-rounded constants).
-// MODE 1: deformation field (build_field, mapping.py:194-204) in float64, with the raw
-// map in the collapsed form  2C tx = tl(1-2y) + up(2x-1) + Gx,  2C ty = tl(1-2x) +
-// up(1-2y) + Gy  (the anchor coefficients of tl and up are constant across the
-// mapping.py:42/47 branches; Gx, Gy carry the marginal terms).
-template <int CPL, int MODE>
+// MODE 1 / 2: deformation field (build_field, mapping.py:194-204), with the raw map in the
+// collapsed form  2C tx = tl(1-2y) + up(2x-1) + Gx,  2C ty = tl(1-2x) + up(1-2y) + Gy
+// (the anchor coefficients of tl and up are constant across the mapping.py:42/47
+// branches; Gx, Gy carry the column / row / diagonal marginals Cp, Rp, Ap, Ds).  Every
+// quantity is normalised by its total (C for the data, s^2 for the flat texture) so the
+// arithmetic is O(1) float32.  Without an explicit defect array the flat response is
+// folded in term by term: the same linear form is evaluated on (data/C - flat/s^2)
+// differences, which are small where the density is near uniform, so the cancellation
+// of raw - defect happens before rounding instead of after (MODE 1); MODE 2 subtracts an
+// explicit defect array (build_field with a caller-supplied flat response).
+// GSRC: `src` is the tile origin in global memory (row stride ld) and rows are fetched
+// two ahead into registers; otherwise `src` is a staged (shared-memory) tile.
+template <int CPL, int MODE, bool GSRC = false>
 __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
                                                 int lane, const WriteOut out) {
-    using T = typename std::conditional<MODE == 0, float, double>::type;
     const int TH = g.TH, TW = g.TW, s = g.s, NX = g.NX, B = g.B;
     const int last = g.WL - 1;
     const int u0 = lane * CPL;
@@ -184,61 +231,82 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
     const int a = b * TH, i0 = x * TW;
     const int64_t tile = (int64_t)b * NX + x;
     const double C = *ws.total;
+    const double invC = 1.0 / C;
+    constexpr bool diff = MODE == 1;  // fold the flat response in
+    const double inv_s = ldexp(1.0, -g.k), inv_s2 = inv_s * inv_s;
     const double* __restrict__ tlc = ws.tlcar + (int64_t)b * s;
     const double* __restrict__ cpre = ws.tlcar + (int64_t)B * s;
     const double* __restrict__ x1 = ws.x1 + (int64_t)b * s;
     const double* __restrict__ x2 = ws.x2 + (int64_t)b * (s + TH);
     const double* __restrict__ apre = ws.apre;
     const double* __restrict__ dsuf = ws.dsuf + (s - 1);  // index by delta = i - j
+    // normalised marginal entries (MODE 1): value / C, minus the flat value when folding
+    auto nap = [&](int sg) {
+        const double v = apre[sg] * invC;
+        return (float)(diff ? v - (double)flat_apre_count(sg, s) * inv_s2 : v);
+    };
+    auto nds = [&](int dl) {
+        const double v = dsuf[dl] * invC;
+        return (float)(diff ? v - (double)flat_dsuf_count(dl, s) * inv_s2 : v);
+    };
     // per-column constants and initial windows (row 0)
-    T A[CPL], Bc[CPL], w1[CPL], w2[CPL], wa[CPL], wd[CPL];
+    float A[CPL], Bc[CPL], w1[CPL], w2[CPL], wa[CPL], wd[CPL];
 #pragma unroll
     for (int e = 0; e < CPL; ++e) {
         const int i = i0 + u0 + e;
         const bool ok = act && i < s;
         const double tv = ok ? tlc[i] : 0.0, cv = ok ? cpre[i] : 0.0;
-        A[e] = (T)tv;
-        Bc[e] = (T)(cv - tv);  // MODE 1 uses Bc = Cp
-        if (MODE == 1) Bc[e] = (T)cv;
-        w1[e] = (T)(ok && i - 1 >= 0 ? x1[i - 1] : 0.0);  // X1[i - r - 1]
-        w2[e] = (T)(ok ? x2[i + 1] : 0.0);                // X2[i + r + 1]
-        wa[e] = (T)(ok ? apre[a + i] : 0.0);              // Apre[i + j]
-        wd[e] = (T)(ok ? dsuf[i - a] : 0.0);              // Dsuf[i - j]
+        A[e] = (float)tv;
+        w1[e] = (float)(ok && i - 1 >= 0 ? x1[i - 1] : 0.0);  // X1[i - r - 1]
+        w2[e] = (float)(ok ? x2[i + 1] : 0.0);                // X2[i + r + 1]
+        if (MODE == 0) {
+            Bc[e] = (float)(cv - tv);
+            wa[e] = (float)(ok ? apre[a + i] : 0.0);  // Apre[i + j]
+            wd[e] = (float)(ok ? dsuf[i - a] : 0.0);  // Dsuf[i - j]
+        } else {
+            Bc[e] = (float)(diff ? cv * invC - (i + 1) * inv_s : cv * invC);  // Cp
+            wa[e] = ok ? nap(a + i) : 0.f;
+            wd[e] = ok ? nds(i - a) : 0.f;
+        }
     }
     // lane-distributed: row constants (lane q = row q) and window / chain edge entries
-    T P = 0, Q = 0, S = 0;
-    double Rp = 0.0;
-    T e1 = 0, e2 = 0, ea = 0, ed = 0;
+    float P = 0, Q = 0, S = 0;
+    float e1 = 0, e2 = 0, ea = 0, ed = 0;
     float ulel = 0.f, urer = 0.f;
     {
         const double hc = lane < TH ? ws.hc[(int64_t)(a + lane) * NX + x] : 0.0;
         const double vh = warp_inclusive_scan_d(hc, lane);
         if (lane < TH) {
-            Rp = ws.rpre[a + lane];
-            P = (T)vh;
-            Q = (T)(Rp - vh);
-            S = (T)(C - Rp + vh);
+            const double Rp = ws.rpre[a + lane];
+            P = (float)vh;
+            if (MODE == 0) {
+                Q = (float)(Rp - vh);
+                S = (float)(C - Rp + vh);
+            } else {
+                Q = (float)(diff ? Rp * invC - (a + lane + 1) * inv_s : Rp * invC);  // Rp
+            }
             if (lane < TH - 1) {  // entry q feeds row q + 1
                 const int c1 = i0 - 2 - lane;
-                e1 = (T)(c1 >= 0 ? x1[c1] : 0.0);
-                e2 = (T)x2[i0 + TW + 1 + lane];
-                ea = (T)apre[a + i0 + TW + lane];
-                ed = (T)dsuf[i0 - a - 1 - lane];
+                e1 = (float)(c1 >= 0 ? x1[c1] : 0.0);
+                e2 = (float)x2[i0 + TW + 1 + lane];
+                ea = MODE == 0 ? (float)apre[a + i0 + TW + lane] : nap(a + i0 + TW + lane);
+                ed = MODE == 0 ? (float)dsuf[i0 - a - 1 - lane] : nds(i0 - a - 1 - lane);
             }
             ulel = x > 0 ? ws.ule[(tile - 1) * TH + lane] : 0.f;
             urer = x < NX - 1 ? ws.ure[(tile + 1) * TH + lane] : 0.f;
         }
     }
-    const T Ct = (T)C;
-    const double inv = 0.5 / C;
-    const double scale = ldexp(1.0, -g.k);
+    const float Ct = (float)C;
+    const float invCf = (float)invC;
+    const float scale = (float)inv_s, invs2f = (float)inv_s2;
+    constexpr float one = diff ? 0.f : 1.f;
     float V[CPL], UL[CPL], UR[CPL];
 #pragma unroll
     for (int e = 0; e < CPL; ++e) V[e] = UL[e] = UR[e] = 0.f;
     float exc = 0.f;
-    // MODE 1 with a precomputed flat response: the row's defect values are fetched one
-    // row ahead so their latency hides behind the previous row's work.
-    const float2* defrow = (MODE == 1 && out.defect && act)
+    // MODE 1 with an explicit defect: the row's values are fetched one row ahead so their
+    // latency hides behind the previous row's work.
+    const float2* defrow = (MODE == 2 && act)
                                ? reinterpret_cast<const float2*>(out.defect) + (int64_t)a * s + i0 + u0
                                : nullptr;
     float2 dnext[CPL];
@@ -246,7 +314,17 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
 #pragma unroll
         for (int e = 0; e < CPL; ++e) dnext[e] = __ldg(defrow + e);
     }
-    for (int r = 0; r < TH; ++r) {
+    float c0[CPL], c1[CPL];  // GSRC: rows r and r + 1 in flight
+    if (GSRC) {
+#pragma unroll
+        for (int e = 0; e < CPL; ++e) c0[e] = c1[e] = 0.f;
+        if (act) {
+            load_row_g<CPL>(src + u0, c0);
+            if (TH > 1) load_row_g<CPL>(src + (size_t)ld + u0, c1);
+        }
+    }
+    // one row of the sweep; GSRC: `cb` holds row r and is refilled with row r + 2
+    auto step = [&](const int r, float (&cb)[CPL]) {
         float2 dcur[CPL];
         if (defrow) {
 #pragma unroll
@@ -257,8 +335,13 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
             }
         }
         float dv[CPL];
-        if (act) load_row<CPL>(src + (size_t)r * ld + u0, dv);
-        else {
+        if (GSRC) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) dv[e] = cb[e];
+            if (act && r + 2 < TH) load_row_g<CPL>(src + (size_t)(r + 2) * ld + u0, cb);
+        } else if (act) {
+            load_row<CPL>(src + (size_t)r * ld + u0, dv);
+        } else {
 #pragma unroll
             for (int e = 0; e < CPL; ++e) dv[e] = 0.f;
         }
@@ -284,9 +367,10 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         for (int e = 1; e < CPL; ++e) loc[e] = loc[e - 1] + V[e];
         const float inc = warp_inclusive_scan(loc[CPL - 1], lane);
         const float off = inc - loc[CPL - 1];
-        const T Pr = __shfl_sync(kFull, P, r);
+        const float Pr = __shfl_sync(kFull, P, r);
+        const float Qr = __shfl_sync(kFull, Q, r);
         if (MODE == 0) {
-            const T Qr = __shfl_sync(kFull, Q, r), Sr = __shfl_sync(kFull, S, r);
+            const float Sr = __shfl_sync(kFull, S, r);
             float o[8][CPL];
 #pragma unroll
             for (int e = 0; e < CPL; ++e) {
@@ -308,43 +392,58 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                 for (int t = 0; t < 8; ++t) store_row_cs<CPL>(out.tables8 + (int64_t)t * g.m + q, o[t]);
             }
         } else {
-            const double Rr = __shfl_sync(kFull, Rp, r);
             const int j = a + r;
-            const double yy = j * scale;
+            const float yy = j * scale, fj = (j + 1) * scale;
+            const float a1 = 1.f - 2.f * yy, omq = one - Qr;
+            const int tj1 = 2 * j + 1;
             float res[2 * CPL];
 #pragma unroll
             for (int e = 0; e < CPL; ++e) {
                 const int i = i0 + u0 + e;
-                const double xx = i * scale;
-                const double L = (double)(off + loc[e]);
-                const double tl = (A[e] + Pr) + L;
-                const double up = (double)(UL[e] + UR[e] - V[e]) + (w1[e] + w2[e]);
-                const double Cp = Bc[e], Ap = wa[e], Ds = wd[e];
-                const bool below = yy < xx, near = xx + yy < 1.0;
-                const double ulx = below ? xx - yy : 0.0, uly = below ? 0.0 : yy - xx;
-                const double urx = near ? xx + yy : 1.0, ury = near ? 0.0 : xx + yy - 1.0;
-                const double dlx = near ? 0.0 : xx + yy - 1.0, dly = near ? xx + yy : 1.0;
-                const double Gx = Cp * (urx - ulx) + (C - Rr) * ulx + Rr * dlx + (C - Ap - Ds) * xx + Ap;
-                const double Gy = Cp * (ury - uly) + (C - Rr) * uly + Rr * dly + (Ap + Ds) * yy;
-                const double tx = (tl * (1.0 - 2.0 * yy) + up * (2.0 * xx - 1.0) + Gx) * inv;
-                const double ty = (tl * (1.0 - 2.0 * xx) + up * (1.0 - 2.0 * yy) + Gy) * inv;
-                double2 def;
-                if (defrow) {
-                    def.x = dcur[e].x;
-                    def.y = dcur[e].y;
-                } else if (out.defect) {
-                    const float2 dfv = reinterpret_cast<const float2*>(out.defect)[(int64_t)j * s + i];
-                    def.x = dfv.x;
-                    def.y = dfv.y;
+                const float xx = i * scale, b1 = 2.f * xx - 1.f;
+                const float tl = (A[e] + Pr) + (off + loc[e]);
+                const float up = (UL[e] + UR[e] - V[e]) + (w1[e] + w2[e]);
+                float tln, upn;
+                if (diff) {
+                    tln = fmaf(tl, invCf, -((i + 1) * scale) * fj);
+                    upn = fmaf(up, invCf, -(float)flat_up_count(i, s - 1 - i, j, tj1) * invs2f);
                 } else {
-                    def = flat_response_at(i, j, g.k);
+                    tln = tl * invCf;
+                    upn = up * invCf;
                 }
-                const float gx = (float)(tx - def.x + xx), gy = (float)(ty - def.y + yy);
+                const float cp = Bc[e], ap = wa[e], ds = wd[e];
+                // anchors (mapping.py:42-47) without branches: x + y and x - y are exact
+                const float sxy = xx + yy;
+                const float ulx = fmaxf(xx - yy, 0.f), uly = fmaxf(yy - xx, 0.f);
+                const float u = fminf(sxy, 1.f), hp = fmaxf(sxy - 1.f, 0.f);  // urx = dly, ury = dlx
+                const float gxs = fmaf(cp, u - ulx, fmaf(omq, ulx, fmaf(Qr, hp, fmaf(one - ap - ds, xx, ap))));
+                const float gys = fmaf(cp, hp - uly, fmaf(omq, uly, fmaf(Qr, u, (ap + ds) * yy)));
+                float gx = fmaf(0.5f, fmaf(tln, a1, fmaf(upn, b1, gxs)), xx);
+                float gy = fmaf(0.5f, fmaf(tln, -b1, fmaf(upn, a1, gys)), yy);
+                if (MODE == 2) {
+                    gx -= dcur[e].x;
+                    gy -= dcur[e].y;
+                }
                 if (act) exc = fmaxf(exc, fmaxf(fmaxf(-gx, -gy), fmaxf(gx - 1.f, gy - 1.f)));
-                res[2 * e] = fminf(fmaxf(gx, 0.f), 1.f);
-                res[2 * e + 1] = fminf(fmaxf(gy, 0.f), 1.f);
+                res[2 * e] = __saturatef(gx);
+                res[2 * e + 1] = __saturatef(gy);
             }
-            if (act) {
+            if (out.pairs) {
+                // paired layout for the move: slot i holds (t(i), t(i + 1)), so the
+                // bilinear footprint is two 16-byte loads.  The half that belongs to
+                // the next tile's first column is written by that tile's warp.
+                const float nx = __shfl_down_sync(kFull, res[0], 1), ny = __shfl_down_sync(kFull, res[1], 1);
+                if (act) {
+                    float4* pd = reinterpret_cast<float4*>(out.pairs) + ((int64_t)j * s + i0 + u0);
+#pragma unroll
+                    for (int e = 0; e < CPL - 1; ++e)
+                        pd[e] = make_float4(res[2 * e], res[2 * e + 1], res[2 * e + 2], res[2 * e + 3]);
+                    if (lane < last) pd[CPL - 1] = make_float4(res[2 * CPL - 2], res[2 * CPL - 1], nx, ny);
+                    else reinterpret_cast<float2*>(pd + CPL - 1)[0] = make_float2(res[2 * CPL - 2], res[2 * CPL - 1]);
+                    if (lane == 0 && i0 > 0) reinterpret_cast<float2*>(pd - 1)[1] = make_float2(res[0], res[1]);
+                }
+            }
+            if (act && out.targets) {
                 float* dst = out.targets + 2 * ((int64_t)j * s + i0 + u0);
                 if constexpr (CPL == 4) {
                     __stcs(reinterpret_cast<float4*>(dst), make_float4(res[0], res[1], res[2], res[3]));
@@ -361,8 +460,12 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         slide_left<CPL>(wd, ed, r, lane);
         slide_right<CPL>(w2, e2, r, lane, last);
         slide_right<CPL>(wa, ea, r, lane, last);
+    };
+    for (int r = 0; r < TH; r += 2) {  // two rows per trip so each prefetch buffer is a fixed register set
+        step(r, c0);
+        if (r + 1 < TH) step(r + 1, c1);
     }
-    if (MODE == 1) {
+    if (MODE != 0) {
         exc = warp_max(exc);
         if (lane == 0 && exc > 0.f) atomic_max_nonneg(out.max_exc, exc);
     }

@@ -61,21 +61,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const __grid_
     warp_tile_reduce<CPL>(slot, g.TW, g, ws, b, x, lane);
 }
 
+// The write pass re-reads its tile straight from global memory (rows prefetched two
+// ahead in registers): no shared memory, so residency is bounded by registers only.
 template <int CPL, int MODE>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) write_kernel(const __grid_constant__ CUtensorMap map,
-                                                                  const float* d, const Geo g, const Ws ws,
-                                                                  const WriteOut out, int use_tma, const int* state) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) write_kernel(const float* __restrict__ d, const Geo g,
+                                                                  const Ws ws, const WriteOut out, const int* state) {
     if (state && state[0]) return;  // displacement stop already reached
-    extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kWarpsPerCta + w;
     if (tile >= g.B * g.NX) return;
     const int b = tile / g.NX, x = tile - b * g.NX;
-    float* slot = reinterpret_cast<float*>(smem) + (size_t)w * g.TH * g.TW;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * (size_t)g.TH * g.TW * sizeof(float)) + w;
-    if (use_tma && lane == 0) prefetch_tensormap(&map);
-    warp_load_tile(slot, bar, &map, d, g, b, x, use_tma, lane);
-    warp_tile_write<CPL, MODE>(slot, g.TW, g, ws, b, x, lane, out);
+    const float* src = d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW;
+    warp_tile_write<CPL, MODE, true>(src, g.s, g, ws, b, x, lane, out);
 }
 
 // ---- standalone helpers --------------------------------------------------------------
@@ -196,19 +193,9 @@ int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const 
 }
 
 template <int CPL, int MODE>
-static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const WriteOut& out,
-                            const int* state, cudaStream_t st) {
-    const size_t smem = tile_smem_bytes(g);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(write_kernel<CPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    const int use_tma = (map != nullptr && tma_ok(g)) ? 1 : 0;
-    CUtensorMap dummy;
-    memset(&dummy, 0, sizeof(dummy));
-    write_kernel<CPL, MODE><<<tile_ctas(g), kWarpsPerCta * 32, smem, st>>>(use_tma ? *map : dummy, d, g, ws, out,
-                                                                          use_tma, state);
+static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const WriteOut& out, const int* state,
+                            cudaStream_t st) {
+    write_kernel<CPL, MODE><<<tile_ctas(g), kWarpsPerCta * 32, 0, st>>>(d, g, ws, out, state);
     prof_mark(st, MODE == 0 ? "write_tables" : "write_field");
     return (int)cudaGetLastError();
 }
@@ -217,22 +204,22 @@ template <int MODE>
 static int launch_write_mode(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const WriteOut& out,
                              const int* state, cudaStream_t st) {
     switch (g.CPL) {
-        case 4: return launch_write_cpl<4, MODE>(d, g, ws, map, out, state, st);
-        case 2: return launch_write_cpl<2, MODE>(d, g, ws, map, out, state, st);
-        default: return launch_write_cpl<1, MODE>(d, g, ws, map, out, state, st);
+        case 4: return launch_write_cpl<4, MODE>(d, g, ws, out, state, st);
+        case 2: return launch_write_cpl<2, MODE>(d, g, ws, out, state, st);
+        default: return launch_write_cpl<1, MODE>(d, g, ws, out, state, st);
     }
 }
 
 int launch_write_tables(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, float* tables8,
                         cudaStream_t st) {
-    WriteOut o{tables8, nullptr, nullptr, nullptr};
+    WriteOut o{tables8, nullptr, nullptr, nullptr, nullptr};
     return launch_write_mode<0>(d, g, ws, map, o, nullptr, st);
 }
 
 int launch_write_field(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const float* defect,
-                       float* targets, float* max_exc, const int* state, cudaStream_t st) {
-    WriteOut o{nullptr, targets, defect, max_exc};
-    return launch_write_mode<1>(d, g, ws, map, o, state, st);
+                       float* targets, float* max_exc, const int* state, cudaStream_t st, float* pairs) {
+    WriteOut o{nullptr, targets, defect, max_exc, pairs};
+    return defect ? launch_write_mode<2>(d, g, ws, map, o, state, st) : launch_write_mode<1>(d, g, ws, map, o, state, st);
 }
 
 int launch_field_from_tables(const float* t8, int k, const double* total, const float* defect, float* targets,

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) unsigned char smem[];
     const Geo& g = A.g;
-    const int s = g.s, k = g.k;
+    const int s = g.s;
     const int64_t m = g.m;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles = g.B * g.NX;
@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
     const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
     const int nH = (s / A.h.TWH) * (s / A.h.RH), nHx = s / A.h.TWH;
     const int nV = g.NX * (s / A.v.VR);
-    const int ncol = colscan_items(g, kMegaWarps), ndiag = diagscan_items(g, kMegaThreads);
-    const int nmarg = marg_items(g, kMegaThreads);
+    const int nchain = chains_items(g), nmarg = marg_entries(g);
+    double(*part)[33] = reinterpret_cast<double(*)[33]>(smem);
+    double* bp = reinterpret_cast<double*>(smem) + kMegaWarps * 33;
+    double* shs = bp + g.B + 1;
     int done = 0;
     for (int t = 0; t < A.iters; ++t) {
         nst = 0;
@@ -135,24 +137,22 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
         grid.sync();
         stamp(t);
         // ---- carry scan
-        for (int b = blockIdx.x; b < g.B; b += gridDim.x) band_rows_item(g, A.ws, b, reinterpret_cast<double*>(smem));
+        for (int b = blockIdx.x; b < g.B; b += gridDim.x) lines_item(g, A.ws, b, shs);
         grid.sync();
         stamp(t);
-        for (int item = blockIdx.x; item < ncol; item += gridDim.x)
-            colscan_item(g, A.ws, item, reinterpret_cast<double(*)[33]>(smem));
+        band_prefix(g, A.ws, bp, shs);  // every CTA: X2 chains need it
+        if (blockIdx.x == 0)
+            for (int q = threadIdx.x; q <= g.B; q += blockDim.x) A.ws.bandpre[q] = bp[q];
+        for (int item = blockIdx.x; item < nchain; item += gridDim.x) chains_item(g, A.ws, item, part, bp);
         grid.sync();
         stamp(t);
-        for (int item = blockIdx.x; item < ndiag; item += gridDim.x)
-            diagscan_item(g, A.ws, item, reinterpret_cast<double(*)[33]>(smem));
-        grid.sync();
-        stamp(t);
-        for (int item = blockIdx.x; item < nmarg; item += gridDim.x) marg_item(g, A.ws, item);
+        for (int64_t q = gtid; q < nmarg; q += gstride) marg_entry(g, A.ws, (int)q);
         grid.sync();
         stamp(t);
         // ---- field: one warp per tile, tile staged by TMA into the warp's slot
         {
             fence_proxy_async_global();
-            const WriteOut out{nullptr, tg, A.defect, exc};
+            const WriteOut out{nullptr, tg, A.defect, exc, nullptr};
             for (int tile = blockIdx.x * kMegaWarps + warp; tile < tiles; tile += gridDim.x * kMegaWarps) {
                 const int b = tile / g.NX, x = tile - b * g.NX;
                 if (lane == 0) {
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
                 __syncwarp();
                 mbar_wait(&bars[warp], parity);
                 parity ^= 1u;
-                warp_tile_write<CPL, 1>(slot, g.TW, g, A.ws, b, x, lane, out);
+                warp_tile_write<CPL, 1, false>(slot, g.TW, g, A.ws, b, x, lane, out);
                 __syncwarp();
             }
         }
@@ -239,7 +239,7 @@ static size_t mega_body_bytes(const Geo& g, const HGeo& h, const VGeo& v, int R)
     b = b > v_smem_bytes(g, v, R) ? b : v_smem_bytes(g, v, R);
     const size_t w = kMegaWarps * (size_t)g.TH * g.TW * sizeof(float);
     b = b > w ? b : w;
-    const size_t sc = sizeof(double) * 33 * kMegaWarps;
+    const size_t sc = sizeof(double) * (33 * kMegaWarps + g.B + 1 + 33);
     b = b > sc ? b : sc;
     return (b + 127) & ~size_t(127);
 }

@@ -2,6 +2,9 @@
 // model.py:189-198) and the bilinear move (mapping.py:207-246 + the clip of
 // regularize.py:36).  Both stream the (n, 2) interleaved positions with 16-byte
 // vector accesses (two points per float4) and touch the grid through L2.
+#include <mutex>
+#include <unordered_map>
+
 #include "inim_points.cuh"
 
 namespace inim {
@@ -29,10 +32,19 @@ __global__ void __launch_bounds__(256) splat_f32_kernel(const float4* __restrict
     const int s = 1 << k;
     const int64_t npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += stride) {
-        const float4 v = __ldcs(pts2 + p);  // streamed: read once per splat
-        atomicAdd(counts + pixel_of(v.y, s) * s + pixel_of(v.x, s), 1u);
-        atomicAdd(counts + pixel_of(v.w, s) * s + pixel_of(v.z, s), 1u);
+    constexpr int U = 4;  // four 16-byte loads in flight per thread before its atomics
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npair; p += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (p + u * stride < npair) v[u] = __ldcs(pts2 + p + u * stride);  // streamed: read once per splat
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (p + u * stride < npair) {
+                atomicAdd(counts + pixel_of(v[u].y, s) * s + pixel_of(v[u].x, s), 1u);
+                atomicAdd(counts + pixel_of(v[u].w, s) * s + pixel_of(v[u].z, s), 1u);
+            }
+        }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const float x = pts[2 * (n - 1)], y = pts[2 * (n - 1) + 1];
@@ -56,53 +68,78 @@ __global__ void __launch_bounds__(256) splat_f64_kernel(const double* __restrict
     }
 }
 
-__global__ void __launch_bounds__(256) sample_f32_kernel(const float2* __restrict__ tg, int k,
+// PAIRS: `tg` is the paired (s, s, 4) field layout (bilinear_pairs), else (s, s, 2).
+template <bool PAIRS>
+__device__ __forceinline__ void move_point(const float* tg, int s, float x, float y, float& ox, float& oy) {
+    if (PAIRS) bilinear_pairs(reinterpret_cast<const float4*>(tg), s, x, y, ox, oy);
+    else bilinear<float>(reinterpret_cast<const float2*>(tg), s, x, y, ox, oy);
+}
+
+template <bool PAIRS>
+__global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict__ tg, int k,
                                                          const float4* __restrict__ in2, const float* __restrict__ in,
                                                          float4* __restrict__ out2, float* __restrict__ out, int64_t n,
-                                                         int clip, float* max_disp, const int* state) {
+                                                         int clip, float* max_disp, const int* state,
+                                                         uint32_t* __restrict__ splat_next, float* zn0, float* zn1) {
     const bool stopped = state && state[0];
     const int s = 1 << k;
+    // fused splat of the next iteration (its count buffer was cleared by this
+    // iteration's smoothing) and the reset of the next iteration's device scalars
+    if (splat_next && !stopped && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (zn0) *zn0 = 0.f;
+        if (zn1) *zn1 = 0.f;
+    }
     const int64_t npair = n >> 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     float md = 0.f;
-    // four points (two 16-byte loads) per thread per step: 16 independent gathers in flight
-    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += 2 * stride) {
-        const int64_t p1 = p0 + stride;
-        const bool has1 = p1 < npair;
-        const float4 v0 = __ldcs(in2 + p0);
-        const float4 v1 = has1 ? __ldcs(in2 + p1) : v0;
-        float4 o0, o1;
-        if (stopped) {
-            o0 = v0;  // keep the ping-pong buffers consistent after a displacement stop
-            o1 = v1;
-        } else {
-            bilinear<float>(tg, s, v0.x, v0.y, o0.x, o0.y);
-            bilinear<float>(tg, s, v0.z, v0.w, o0.z, o0.w);
-            bilinear<float>(tg, s, v1.x, v1.y, o1.x, o1.y);
-            bilinear<float>(tg, s, v1.z, v1.w, o1.z, o1.w);
-            if (clip) {
-                o0.x = clip01(o0.x); o0.y = clip01(o0.y); o0.z = clip01(o0.z); o0.w = clip01(o0.w);
-                o1.x = clip01(o1.x); o1.y = clip01(o1.y); o1.z = clip01(o1.z); o1.w = clip01(o1.w);
-            }
-            md = fmaxf(md, fmaxf(fmaxf(fabsf(o0.x - v0.x), fabsf(o0.y - v0.y)),
-                                 fmaxf(fabsf(o0.z - v0.z), fabsf(o0.w - v0.w))));
-            if (has1)
-                md = fmaxf(md, fmaxf(fmaxf(fabsf(o1.x - v1.x), fabsf(o1.y - v1.y)),
-                                     fmaxf(fabsf(o1.z - v1.z), fabsf(o1.w - v1.w))));
+    // U pairs of points (U 16-byte loads) per thread per step, all gathers in flight
+    constexpr int U = 2;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += U * stride) {
+        float4 v[U], o[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = p0 + u * stride;
+            v[u] = q < npair ? __ldcs(in2 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        __stcs(out2 + p0, o0);
-        if (has1) __stcs(out2 + p1, o1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (stopped) {
+                o[u] = v[u];  // keep the ping-pong buffers consistent after a displacement stop
+                continue;
+            }
+            move_point<PAIRS>(tg, s, v[u].x, v[u].y, o[u].x, o[u].y);
+            move_point<PAIRS>(tg, s, v[u].z, v[u].w, o[u].z, o[u].w);
+            if (clip) {
+                o[u].x = clip01(o[u].x); o[u].y = clip01(o[u].y); o[u].z = clip01(o[u].z); o[u].w = clip01(o[u].w);
+            }
+            if (p0 + u * stride < npair)
+                md = fmaxf(md, fmaxf(fmaxf(fabsf(o[u].x - v[u].x), fabsf(o[u].y - v[u].y)),
+                                     fmaxf(fabsf(o[u].z - v[u].z), fabsf(o[u].w - v[u].w))));
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (p0 + u * stride < npair) __stcs(out2 + p0 + u * stride, o[u]);
+        if (splat_next && !stopped) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (p0 + u * stride < npair) {
+                    atomicAdd(splat_next + pixel_of(o[u].y, s) * s + pixel_of(o[u].x, s), 1u);
+                    atomicAdd(splat_next + pixel_of(o[u].w, s) * s + pixel_of(o[u].z, s), 1u);
+                }
+            }
+        }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const float x = in[2 * (n - 1)], y = in[2 * (n - 1) + 1];
         float ox = x, oy = y;
         if (!stopped) {
-            bilinear<float>(tg, s, x, y, ox, oy);
+            move_point<PAIRS>(tg, s, x, y, ox, oy);
             if (clip) { ox = clip01(ox); oy = clip01(oy); }
             md = fmaxf(md, fmaxf(fabsf(ox - x), fabsf(oy - y)));
         }
         out[2 * (n - 1)] = ox;
         out[2 * (n - 1) + 1] = oy;
+        if (splat_next && !stopped) atomicAdd(splat_next + pixel_of(oy, s) * s + pixel_of(ox, s), 1u);
     }
     if (max_disp && !stopped) {
         md = warp_max(md);
@@ -250,6 +287,30 @@ static int sm_count() {
     return n;
 }
 
+// Grid of at most one full wave: blocks x threads covers `work` items (capped at what is
+// co-resident on all SMs given the kernel's registers / shared memory).
+static unsigned resident_grid(const void* kernel, int64_t work, int threads, size_t smem = 0) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> occ;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = occ.find(kernel);
+        if (it == occ.end()) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess ||
+                per_sm < 1)
+                per_sm = 1;
+            occ[kernel] = per_sm;
+        } else {
+            per_sm = it->second;
+        }
+    }
+    int64_t blocks = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
 static unsigned grid_for(int64_t work, int per_block) {
     int64_t blocks = (work + per_block - 1) / per_block;
     const int64_t cap = (int64_t)sm_count() * 8;  // 8 resident 256-thread CTAs per SM
@@ -299,11 +360,12 @@ int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cuda
 }
 
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
-                      const int* state, cudaStream_t st) {
+                      const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1) {
     const int64_t npair = n >> 1;
-    sample_f32_kernel<<<grid_for(npair > 0 ? npair : 1, 256), 256, 0, st>>>(
-        reinterpret_cast<const float2*>(tg), k, reinterpret_cast<const float4*>(in), in,
-        reinterpret_cast<float4*>(out), out, n, clip, max_disp, state);
+    auto kern = pairs ? sample_f32_kernel<true> : sample_f32_kernel<false>;
+    kern<<<resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), 256, 0, st>>>(
+        tg, k, reinterpret_cast<const float4*>(in), in, reinterpret_cast<float4*>(out), out, n, clip, max_disp, state,
+        splat_next, zn0, zn1);
     prof_mark(st, "sample");
     return (int)cudaGetLastError();
 }

@@ -1,43 +1,45 @@
 // Carry scan launches (phase 2 of the integral pass; the item bodies and their
-// derivation are in inim_scan.cuh).  Four launches over 1/TH of the texture, none of
-// which waits on another CTA.
+// derivation are in inim_scan.cuh): lines -> chains -> marg, three launches over
+// 1/TH of the texture, none of which waits on another CTA.
 #include "inim_scan.cuh"
 
 namespace inim {
 
-constexpr int kScanThreads = 256;
+constexpr int kLineThreads = 256;
+constexpr int kMargThreads = 256;
 
-__global__ void __launch_bounds__(kScanThreads) band_rows_kernel(const Geo g, const Ws ws, const int* state) {
+__global__ void __launch_bounds__(kLineThreads) lines_kernel(const Geo g, const Ws ws, const int* state) {
     if (state && state[0]) return;
     __shared__ double sh[33];
-    band_rows_item(g, ws, blockIdx.x, sh);
+    lines_item(g, ws, blockIdx.x, sh);
 }
 
-__global__ void __launch_bounds__(kScanThreads) colscan_kernel(const Geo g, const Ws ws, const int* state) {
+__global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws, const int* state) {
     if (state && state[0]) return;
-    __shared__ double part[kScanThreads / 32][33];
-    colscan_item(g, ws, blockIdx.x, part);
+    __shared__ double part[16][33];
+    __shared__ double bp[kMaxBands + 1];
+    __shared__ double sh[33];
+    const int item = blockIdx.x;
+    if (chain_kind(g, item) == 2) {
+        band_prefix(g, ws, bp, sh);
+        if (item == chain_groups_tl(g) + chain_groups_x(g))  // first X2 item publishes it for marg
+            for (int q = threadIdx.x; q <= g.B; q += blockDim.x) ws.bandpre[q] = bp[q];
+    }
+    chains_item(g, ws, item, part, bp);
 }
 
-__global__ void __launch_bounds__(kScanThreads) diagscan_kernel(const Geo g, const Ws ws, const int* state) {
+__global__ void __launch_bounds__(kMargThreads) marg_kernel(const Geo g, const Ws ws, const int* state) {
     if (state && state[0]) return;
-    __shared__ double part[kScanThreads / 32][33];
-    diagscan_item(g, ws, blockIdx.x, part);
-}
-
-__global__ void __launch_bounds__(kScanThreads) marg_kernel(const Geo g, const Ws ws, const int* state) {
-    if (state && state[0]) return;
-    marg_item(g, ws, blockIdx.x);
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < marg_entries(g)) marg_entry(g, ws, q);
 }
 
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st) {
-    band_rows_kernel<<<g.B, kScanThreads, 0, st>>>(g, ws, state);
-    prof_mark(st, "band_rows");
-    colscan_kernel<<<colscan_items(g, kScanThreads / 32), kScanThreads, 0, st>>>(g, ws, state);
-    prof_mark(st, "colscan");
-    diagscan_kernel<<<diagscan_items(g, kScanThreads), kScanThreads, 0, st>>>(g, ws, state);
-    prof_mark(st, "diagscan");
-    marg_kernel<<<marg_items(g, kScanThreads), kScanThreads, 0, st>>>(g, ws, state);
+    lines_kernel<<<g.B, kLineThreads, 0, st>>>(g, ws, state);
+    prof_mark(st, "lines");
+    chains_kernel<<<chains_items(g), 32 * chain_warps(g), 0, st>>>(g, ws, state);
+    prof_mark(st, "chains");
+    marg_kernel<<<(marg_entries(g) + kMargThreads - 1) / kMargThreads, kMargThreads, 0, st>>>(g, ws, state);
     prof_mark(st, "marg");
     return (int)cudaGetLastError();
 }

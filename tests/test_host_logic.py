@@ -154,3 +154,15 @@ def test_oracle_not_imported_by_product():
     for path in (ROOT / "paper_2408_06513_b200").rglob("*.py"):
         text = path.read_text()
         assert "oracle" not in text.replace("oracles.py", "").lower() or "no oracle" in text.lower(), path
+
+
+def test_generated_taps_match_oracle_kernel(oracle):
+    """csrc/inim_taps.cuh (FFMA-immediate taps) is current and equals the oracle's
+    smoothing_kernel rounded to float32 (density.py:30-37)."""
+    import sys
+    sys.path.insert(0, str(ROOT / "tools"))
+    import gen_taps
+    assert gen_taps.OUT.read_text() == gen_taps.render(), "run tools/gen_taps.py"
+    for ks in (1, 2, 5, 8, 16):
+        ref = np.asarray(oracle.smoothing_kernel(ks), dtype=np.float64).astype(np.float32)
+        np.testing.assert_array_equal(gen_taps.taps(ks), ref)

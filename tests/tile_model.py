@@ -69,31 +69,40 @@ def model_tables(d: np.ndarray, TH: int | None = None, TW: int | None = None):
             rq = TH - 1 - (TW - u)
             if x < NX - 1 and rq >= 0:
                 urb2[b, c] += ure[b, x + 1, rq]
-    batl = np.cumsum(colsum, axis=1)
+    # band-local row prefix of the column sums, as the device forms it: tile-level
+    # exclusive prefix of the tile totals + the in-tile prefix written by the reduce
+    inpre = np.zeros((B, s))
+    tiletot = np.zeros((B, NX))
+    for b in range(B):
+        for x in range(NX):
+            seg = colsum[b, x * TW:(x + 1) * TW]
+            inpre[b, x * TW:(x + 1) * TW] = np.cumsum(seg)
+            tiletot[b, x] = seg.sum()
+    tilepre = np.concatenate([np.zeros((B, 1)), np.cumsum(tiletot, axis=1)[:, :-1]], axis=1)
+    batl = tilepre[:, np.arange(s) // TW] + inpre
+    bandpre = np.concatenate([[0.0], np.cumsum(tiletot.sum(axis=1))])  # TLcar_b[s-1]
     tlcar = np.vstack([np.zeros((1, s)), np.cumsum(batl, axis=0)])
 
-    def TL(b, c):
-        return tlcar[b, c] if c >= 0 else 0.0
-
-    ulcar = np.zeros((B + 1, s))
-    urcar = np.zeros((B + 1, s))
+    # X1 = ULcar - TLcar and X2 = URcar + TLcar[c-1] as sheared scans of band-local terms:
+    #   X1_{b+1}[c] = X1_b[c-TH] + ULbot2_b[c] - batl_b[c]
+    #   X2_{b+1}[c] = X2_b[c+TH] + URbot2_b[c] + batl_b[c-1],  X2_b[c >= s] = TLcar_b[s-1]
+    X1 = np.zeros((B + 1, s))
+    X2 = np.zeros((B + 1, s))
     for b in range(B):
         for c in range(s):
-            prev = ulcar[b, c - TH] if c - TH >= 0 else 0.0
-            ulcar[b + 1, c] = ulb2[b, c] + TL(b, c) - TL(b, c - TH) + prev
-            prevr = urcar[b, c + TH] if c + TH < s else 0.0
-            urcar[b + 1, c] = urb2[b, c] + TL(b, min(c + TH - 1, s - 1)) - TL(b, c - 1) + prevr
-    x1 = ulcar[:B] - tlcar[:B]
+            X1[b + 1, c] = (X1[b, c - TH] if c - TH >= 0 else 0.0) + ulb2[b, c] - batl[b, c]
+            X2[b + 1, c] = ((X2[b, c + TH] if c + TH < s else bandpre[b]) + urb2[b, c]
+                            + (batl[b, c - 1] if c >= 1 else 0.0))
+    x1 = X1[:B]
     x2 = np.zeros((B, s + TH))
     for b in range(B):
-        for c in range(s):
-            x2[b, c] = urcar[b, c] + TL(b, c - 1)
-        x2[b, s:] = tlcar[b, s - 1]
+        x2[b, :s] = X2[b]
+        x2[b, s:] = bandpre[b]
     hc = np.concatenate([np.zeros((s, 1)), np.cumsum(rowsum, axis=1)[:, :-1]], axis=1)
     rtot = rowsum.sum(axis=1)
-    rpre = np.cumsum(rtot)
+    rpre = np.array([bandpre[j // TH] + rtot[(j // TH) * TH:j + 1].sum() for j in range(s)])
     cpre = tlcar[B]
-    C = rpre[-1]
+    C = bandpre[B]
     # diagonal / anti-diagonal marginals from the chains (no per-tile partial sums):
     #   Dsuf[delta>=0] = UL[s-1-delta][s-1],  Dsuf[delta<0] = UL[s-1][s-1+delta] + C - Cpre[s-1+delta]
     #   Apre[sigma<s]  = UR[sigma][0],        Apre[sigma>=s] = UR[s-1][sigma-s+1] + Cpre[sigma-s]
@@ -105,17 +114,15 @@ def model_tables(d: np.ndarray, TH: int | None = None, TW: int | None = None):
             j = s - 1 - delta
             b, r = divmod(j, TH)
             c2 = s - 2 - r
-            dsuf[q] = ule[b, NX - 1, r] + tlcar[b, s - 1] + (x1[b, c2] if c2 >= 0 else 0.0)
+            dsuf[q] = ule[b, NX - 1, r] + bandpre[b] + (x1[b, c2] if c2 >= 0 else 0.0)
         else:
-            c = s - 1 + delta
-            dsuf[q] = ulcar[B, c] + C - cpre[c]
+            dsuf[q] = X1[B, s - 1 + delta] + C           # ULrow + C - Cpre
         sigma = q
         if sigma < s:
             b, r = divmod(sigma, TH)
             apre[q] = ure[b, 0, r] + x2[b, r + 1]
         else:
-            i = sigma - (s - 1)
-            apre[q] = urcar[B, i] + cpre[i - 1]
+            apre[q] = X2[B, sigma - (s - 1)]             # URrow + Cpre
     # ---- write
     out = np.zeros((8, s, s))
     for b in range(B):

@@ -21,9 +21,13 @@ def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "iter"
     lib = _lib.load()
     dev = torch.device("cuda", 0)
-    if mode == "iter":
-        host = four_cluster()
-        n, k = len(host), 10
+    if mode in ("iter", "iter3"):
+        if mode == "iter3":  # 16M points / 4096^2
+            from bench import c3_points
+            host, k = c3_points(16_000_000), 12
+        else:
+            host, k = four_cluster(), 10
+        n = len(host)
         pts = torch.from_numpy(host.astype(np.float32)).to(dev)
         ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev)
         for _ in range(2):
