@@ -50,8 +50,18 @@ static bool use_mega(const Geo& g, int ks) {
 }
 static unsigned long long* g_stamps = nullptr;  // set by inim_run_stamped
 
+bool pdl_enabled() {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("INIM_PDL");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return env == 1;
+}
+
 // Per-iteration bookkeeping for the displacement criterion (regularize.py:76-79).
 __global__ void iter_end_kernel(const float* disp, float eps, int* state) {
+    pdl_enter();
     if (state[0]) return;
     state[1] += 1;
     if (*disp < eps) state[0] = 1;
@@ -132,7 +142,7 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
                                    chain.next_disp);
     if (rc) return rc;
     if (flag) {
-        iter_end_kernel<<<1, 1, 0, st>>>(disp, stop_eps, state);
+        INIM_CUDA_TRY(launch_pdl(iter_end_kernel, dim3(1), dim3(1), 0, st, (const float*)disp, stop_eps, state));
         prof_mark(st, "iter_end");
     }
     return (int)cudaGetLastError();
@@ -190,8 +200,10 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         if (rc) return rc;
         mp = &map;
     }
-    // once per run: both count buffers cleared, the flat response laid out
+    // once per run: both count buffers cleared (the smoothing of each iteration clears
+    // the reduce's band counters; the persistent kernel relies on this memset)
     INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * 2 * g.m, st));
+    INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, st));
     prof_mark(st, "memset_counts");
     if (defect) {
         int rc = launch_flat_response(g.k, defect, st);
@@ -293,6 +305,7 @@ int inim_integral_set(const float* d, int k, float* tables8, double* total, void
         if (rc) return rc;
         mp = &map;
     }
+    INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, stream));  // reduce's band counters
     int rc = launch_reduce_from_global(d, g, w, mp, stream);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, w, nullptr, stream);
@@ -328,6 +341,7 @@ int inim_field_from_density(const float* d, int k, const float* defect, float* t
         if (rc) return rc;
         mp = &map;
     }
+    INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, stream));  // reduce's band counters
     int rc = launch_reduce_from_global(d, g, w, mp, stream);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, w, nullptr, stream);

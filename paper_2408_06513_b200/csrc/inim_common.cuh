@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/inim.h"
 
 #define INIM_DEV __device__ __forceinline__
@@ -121,10 +123,43 @@ INIM_DEV void st_stream2(float2* p, float2 v) {
     asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
 
-}  // namespace inim
 
 #define INIM_CUDA_TRY(expr)                                       \
     do {                                                          \
         cudaError_t _e = (expr);                                  \
         if (_e != cudaSuccess) return static_cast<int>(_e);       \
     } while (0)
+
+// ---------------------------------------------------- programmatic dependent launch
+// Kernels of the iteration chain are launched with programmatic stream serialisation:
+// a kernel's CTAs may be scheduled while its predecessor drains, and every kernel first
+// waits (griddepcontrol.wait: the predecessor grid has completed and its writes are
+// visible) and then lets its own successor start launching.  The wait is the kernel's
+// first statement, before any early exit, so completion stays transitive along the
+// chain.  Without the launch attribute both instructions are no-ops.
+INIM_DEV void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef INIM_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+bool pdl_enabled();  // abi.cu: INIM_PDL=0 disables
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+}  // namespace inim

@@ -12,6 +12,7 @@ namespace inim {
 
 struct Geo {
     int k, s, TH, TW, B, NX, NW, WL, CPL;  // WL = lanes holding columns; CPL = columns per lane
+    int twlog;                             // log2(TW)
     int64_t m;
 };
 
@@ -31,6 +32,8 @@ inline Geo make_geo(int k) {
     g.NX = g.s / g.TW;
     g.NW = 1;
     g.WL = g.TW >= 32 ? 32 : g.TW;
+    g.twlog = 0;
+    while ((1 << g.twlog) < g.TW) ++g.twlog;
     return g;
 }
 
@@ -47,13 +50,12 @@ struct WsLayout {
     size_t tilepre;  // double [B][NX]         exclusive prefix over tiles of the tile totals
     size_t btot;     // double [B]             band totals
     size_t bandpre;  // double [B+1]           exclusive prefix of the band totals (TLcar_b[s-1])
-    size_t tlcar;    // double [B+1][s]        rect_tl at the row above each band (row s-1 for b=B)
-    size_t x1;       // double [B+1][s]        ULcar - TLcar (row B: along the last row)
-    size_t x2;       // double [B+1][s+TH]     URcar + TLcar[c-1], extended with TLcar[s-1]
+    size_t tlcar;    // float [B+1][s]         rect_tl at the row above each band (row s-1 for b=B)
+    size_t x1;       // float [B+1][s]         ULcar - TLcar (row B: along the last row)
+    size_t x2;       // float [B+1][s+TH]      URcar + TLcar[c-1], extended with TLcar[s-1]
     size_t hc;       // double [s][NX]         row prefix of d up to each tile's first column
-    size_t rpre;     // double [s]             in-band row prefix, then Rpre
-    size_t apre;     // double [2s-1]          prefix of anti-diagonal totals
-    size_t dsuf;     // double [2s-1]          suffix of diagonal totals
+    size_t rpre;     // double [s]             in-band inclusive prefix of the row totals
+    size_t bandctr;  // uint32 [B]             tiles reduced per band (self-resetting)
     size_t total;    // double [1]
     size_t misc;     // float [16]             scratch scalars
     size_t bytes;
@@ -81,13 +83,12 @@ inline WsLayout make_layout(const Geo& g) {
     L.tilepre = take(sizeof(double) * B * NX);
     L.btot = take(sizeof(double) * B);
     L.bandpre = take(sizeof(double) * (B + 1));
-    L.tlcar = take(sizeof(double) * (B + 1) * s);
-    L.x1 = take(sizeof(double) * (B + 1) * s);
-    L.x2 = take(sizeof(double) * (B + 1) * (s + TH));
+    L.tlcar = take(sizeof(float) * (B + 1) * s);
+    L.x1 = take(sizeof(float) * (B + 1) * s);
+    L.x2 = take(sizeof(float) * (B + 1) * (s + TH));
     L.hc = take(sizeof(double) * s * NX);
     L.rpre = take(sizeof(double) * s);
-    L.apre = take(sizeof(double) * (2 * s - 1));
-    L.dsuf = take(sizeof(double) * (2 * s - 1));
+    L.bandctr = take(sizeof(uint32_t) * B);
     L.total = take(sizeof(double));
     L.misc = take(sizeof(float) * 16);
     L.bytes = o;
@@ -107,13 +108,12 @@ struct Ws {
     double* tilepre;
     double* btot;
     double* bandpre;
-    double* tlcar;
-    double* x1;
-    double* x2;
+    float* tlcar;  // carries: float64 scans, stored float32 (the write pass computes in float32)
+    float* x1;
+    float* x2;
     double* hc;
     double* rpre;
-    double* apre;
-    double* dsuf;
+    uint32_t* bandctr;
     double* total;
     float* misc;
 };
@@ -132,13 +132,12 @@ inline Ws make_ws(void* base, const WsLayout& L) {
     w.tilepre = reinterpret_cast<double*>(b + L.tilepre);
     w.btot = reinterpret_cast<double*>(b + L.btot);
     w.bandpre = reinterpret_cast<double*>(b + L.bandpre);
-    w.tlcar = reinterpret_cast<double*>(b + L.tlcar);
-    w.x1 = reinterpret_cast<double*>(b + L.x1);
-    w.x2 = reinterpret_cast<double*>(b + L.x2);
+    w.tlcar = reinterpret_cast<float*>(b + L.tlcar);
+    w.x1 = reinterpret_cast<float*>(b + L.x1);
+    w.x2 = reinterpret_cast<float*>(b + L.x2);
     w.hc = reinterpret_cast<double*>(b + L.hc);
     w.rpre = reinterpret_cast<double*>(b + L.rpre);
-    w.apre = reinterpret_cast<double*>(b + L.apre);
-    w.dsuf = reinterpret_cast<double*>(b + L.dsuf);
+    w.bandctr = reinterpret_cast<uint32_t*>(b + L.bandctr);
     w.total = reinterpret_cast<double*>(b + L.total);
     w.misc = reinterpret_cast<float*>(b + L.misc);
     return w;

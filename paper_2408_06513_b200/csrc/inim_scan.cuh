@@ -53,45 +53,6 @@ __device__ __forceinline__ double block_excl_scan(double v, double* sh /* 33 */,
     return r;
 }
 
-// Exclusive prefix of a line of n values (one warp, float64); returns the line total.
-template <typename T>
-__device__ __forceinline__ double warp_line_prefix(const T* __restrict__ src, double* __restrict__ dst, int n,
-                                                   int lane) {
-    double carry = 0.0;
-    for (int base = 0; base < n; base += 32) {
-        const int x = base + lane;
-        const double v = x < n ? (double)src[x] : 0.0;
-        const double inc = warp_inclusive_scan_d(v, lane);
-        if (x < n) dst[x] = carry + inc - v;
-        carry += __shfl_sync(kFull, inc, 31);
-    }
-    return carry;
-}
-
-__device__ __forceinline__ void lines_item(const Geo& g, const Ws& ws, int b, double* sh /* 33 */) {
-    const int TH = g.TH, NX = g.NX;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int a = b * TH;
-    for (int q = w; q <= TH; q += nw) {
-        if (q < TH) {
-            const int64_t j = a + q;
-            const double tot = warp_line_prefix(ws.rowsum + j * NX, ws.hc + j * NX, NX, lane);
-            if (lane == 0) sh[q] = tot;
-        } else {
-            const double tot =
-                warp_line_prefix(ws.tiletot + (int64_t)b * NX, ws.tilepre + (int64_t)b * NX, NX, lane);
-            if (lane == 0) ws.btot[b] = tot;
-        }
-    }
-    __syncthreads();
-    if (w == 0) {
-        const double v = lane < TH ? sh[lane] : 0.0;
-        const double inc = warp_inclusive_scan_d(v, lane);
-        if (lane < TH) ws.rpre[a + lane] = inc;  // in-band prefix; marg adds TLcar_b[s-1]
-    }
-    __syncthreads();
-}
-
 // Exclusive prefix of the band totals into shared memory bp[0..B] (whole CTA).
 __device__ __forceinline__ void band_prefix(const Geo& g, const Ws& ws, double* bp, double* sh /* 33 */) {
     const int B = g.B;
@@ -121,25 +82,47 @@ __host__ __device__ inline int chain_warps(const Geo& g) {
     return ny < 1 ? 1 : (ny > 16 ? 16 : ny);
 }
 
+// One chain: its band range [lo, hi] (bands whose value is stored or whose step term
+// is non-zero), the step terms and the stores.  Columns: TL c = kk; X1 c_b = kk -
+// (B - b) TH (moves right); X2 c_b = kk - b TH (moves left).
 template <int KIND>
-struct ChainTerms {
+struct Chain {
     const Geo& g;
     const Ws& ws;
     const double* bp;
-    int kk;
+    int kk, lo, hi;
+    __device__ __forceinline__ Chain(const Geo& g_, const Ws& ws_, const double* bp_, int kk_)
+        : g(g_), ws(ws_), bp(bp_), kk(kk_) {
+        const int s = g.s, B = g.B, TH = g.TH;
+        if (KIND == 0) {
+            lo = 0;
+            hi = B;
+        } else if (KIND == 1) {  // col(b) in [0, s) for b in [e0, e1]; terms for b in [e0 - 1, e1 - 1]
+            const int kap = kk - B * TH;
+            const int e0 = kap >= 0 ? 0 : (-kap + TH - 1) / TH;
+            const int e1 = s - 1 - kap < 0 ? -1 : min(B, (s - 1 - kap) / TH);
+            lo = max(0, e0 - 1);
+            hi = e1;
+        } else {  // col(b) in [0, s) for b in [f0, f1]; the entry step / border store at f0 - 1
+            const int f0 = kk <= s - 1 ? 0 : (kk - s + TH) / TH;
+            const int f1 = min(B, kk / TH);
+            lo = max(0, f0 - 1);
+            hi = f1;
+        }
+    }
     __device__ __forceinline__ int col(int b) const {
         return KIND == 0 ? kk : (KIND == 1 ? kk - (g.B - b) * g.TH : kk - b * g.TH);
     }
     __device__ __forceinline__ double batl(int b, int c) const {
-        return ws.tilepre[(int64_t)b * g.NX + c / g.TW] + (double)ws.inpre[(int64_t)b * g.s + c];
+        return ws.tilepre[(int64_t)b * g.NX + (c >> g.twlog)] + (double)ws.inpre[(int64_t)b * g.s + c];
     }
-    // step b -> b + 1
+    // step b -> b + 1 (b < B)
     __device__ __forceinline__ double term(int b) const {
         const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX;
         if (KIND == 0) return batl(b, kk);
         const int c = col(b + 1);
         if (c < 0 || c >= s) return 0.0;
-        const int x = c / TW, u = c - x * TW;
+        const int x = c >> g.twlog, u = c & (TW - 1);
         if (KIND == 1) {
             double v = (double)ws.ulbot[(int64_t)b * s + c] - batl(b, c);
             const int rr = TH - 2 - u;  // row where the chain leaves the tile on the left
@@ -156,45 +139,48 @@ struct ChainTerms {
         const int s = g.s, TH = g.TH;
         const int c = col(b);
         if (KIND == 0) {
-            ws.tlcar[(int64_t)b * s + c] = run;
+            ws.tlcar[(int64_t)b * s + c] = (float)run;
         } else if (KIND == 1) {
-            if (c >= 0 && c < s) ws.x1[(int64_t)b * s + c] = run;
+            if (c >= 0 && c < s) ws.x1[(int64_t)b * s + c] = (float)run;
         } else {
-            if (c >= 0 && c < s) ws.x2[(int64_t)b * (s + TH) + c] = run;
-            else if (c >= s && c < s + TH) ws.x2[(int64_t)b * (s + TH) + c] = bp[b];
+            if (c >= 0 && c < s) ws.x2[(int64_t)b * (s + TH) + c] = (float)run;
+            else if (c >= s && c < s + TH) ws.x2[(int64_t)b * (s + TH) + c] = (float)bp[b];
         }
     }
 };
 
+// 32 chains (lanes) x NY chunks of each chain's band range (warps); two passes: chunk
+// sums, then the scan with stores.
 template <int KIND>
 __device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, double (*part)[33], const double* bp) {
     const int B = g.B;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, NY = blockDim.x >> 5;
     const bool live = kk < (KIND == 0 ? g.s : g.s + B * g.TH);
-    const int CH = (B + NY - 1) / NY;
-    const int b0 = min(B, ty * CH), b1 = min(B, b0 + CH);
-    const ChainTerms<KIND> T{g, ws, bp, kk};
+    const Chain<KIND> T(g, ws, bp, kk);
+    const int len = live && T.hi >= T.lo ? T.hi - T.lo + 1 : 0;  // bands lo..hi (hi may be B: store only)
+    const int CH = (len + NY - 1) / NY;
+    const int b0 = T.lo + min(len, ty * CH), b1 = T.lo + min(len, ty * CH + CH);  // [b0, b1)
+    const int tb1 = min(b1, B);  // step terms exist for b < B
     constexpr int U = 4;  // terms in flight per thread
     double loc = 0.0;
-    if (live) {
+    {
         int b = b0;
-        for (; b + U <= b1; b += U) {
+        for (; b + U <= tb1; b += U) {
             double t[U];
 #pragma unroll
             for (int q = 0; q < U; ++q) t[q] = T.term(b + q);
 #pragma unroll
             for (int q = 0; q < U; ++q) loc += t[q];
         }
-        for (; b < b1; ++b) loc += T.term(b);
+        for (; b < tb1; ++b) loc += T.term(b);
     }
     part[ty][tx] = loc;
     __syncthreads();
     double run = 0.0;
     for (int q = 0; q < ty; ++q) run += part[q][tx];
     __syncthreads();  // `part` is reused by the caller's next item
-    if (!live) return;
     int b = b0;
-    for (; b + U <= b1; b += U) {
+    for (; b + U <= tb1; b += U) {
         double t[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) t[q] = T.term(b + q);
@@ -206,9 +192,8 @@ __device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, 
     }
     for (; b < b1; ++b) {
         T.emit(b, run);
-        run += T.term(b);
+        if (b < B) run += T.term(b);
     }
-    if (b1 == B && b0 < b1) T.emit(B, run);  // the last chunk emits band B too
 }
 
 // bp: the band prefix (band_prefix) for X2 items, else unused.
@@ -219,35 +204,6 @@ __device__ __forceinline__ void chains_item(const Geo& g, const Ws& ws, int item
     if (item < ntl) chains_body<0>(g, ws, item * 32 + tx, part, bp);
     else if (item < ntl + nxg) chains_body<1>(g, ws, (item - ntl) * 32 + tx, part, bp);
     else chains_body<2>(g, ws, (item - ntl - nxg) * 32 + tx, part, bp);
-}
-
-__host__ __device__ inline int marg_entries(const Geo& g) { return 2 * g.s - 1; }
-
-// One entry q of the marginals (q < 2s - 1); bandpre must be complete.
-__device__ __forceinline__ void marg_entry(const Geo& g, const Ws& ws, int q) {
-    const int s = g.s, TH = g.TH, NX = g.NX, B = g.B;
-    const double* __restrict__ bandpre = ws.bandpre;
-    const double C = bandpre[B];
-    if (q == 0) *ws.total = C;
-    if (q < s) ws.rpre[q] += bandpre[q / TH];  // in-band prefix -> Rpre
-    const int delta = q - (s - 1);
-    double dv;
-    if (delta >= 0) {
-        const int j = s - 1 - delta, b = j / TH, r = j - b * TH, c2 = s - 2 - r;
-        dv = (double)ws.ule[((int64_t)b * NX + NX - 1) * TH + r] + bandpre[b] +
-             (c2 >= 0 ? ws.x1[(int64_t)b * s + c2] : 0.0);
-    } else {
-        dv = ws.x1[(int64_t)B * s + s - 1 + delta] + C;
-    }
-    ws.dsuf[q] = dv;
-    double av;
-    if (q < s) {
-        const int b = q / TH, r = q - b * TH;
-        av = (double)ws.ure[(int64_t)b * NX * TH + r] + ws.x2[(int64_t)b * (s + TH) + r + 1];
-    } else {
-        av = ws.x2[(int64_t)B * (s + TH) + q - (s - 1)];
-    }
-    ws.apre[q] = av;
 }
 
 }  // namespace inim

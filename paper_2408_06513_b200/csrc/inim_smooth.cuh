@@ -187,15 +187,12 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
         const int rb = grp * TH;  // first row of this group's band within the CTA
         fir_line<R, 8>(
             taps, TH, [&](int q) { return sh[(rb + q) * TW + tid]; },
-            [&](int p, float val) {
-                const float dv = val + background;
-                sd[(rb + p) * TW + tid] = dv;
-                d[(int64_t)(a0 + rb + p) * s + i0 + tid] = dv;
-            });
+            [&](int p, float val) { sd[(rb + p) * TW + tid] = val + background; });
     }
     __syncthreads();
     if (emit) {
-        // one warp per band tile of d, straight from shared memory
+        // one warp per band tile of d, straight from shared memory; the reduce runs before
+        // this CTA stores d so its band-counter fence only waits on the aggregates
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
         for (int gb = warp; gb < v.VB; gb += nwarps) {
             const float* src = sd + (size_t)gb * TH * TW;
@@ -203,6 +200,19 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
             if (g.CPL == 4) warp_tile_reduce<4>(src, TW, g, ws, b, x, lane);
             else if (g.CPL == 2) warp_tile_reduce<2>(src, TW, g, ws, b, x, lane);
             else warp_tile_reduce<1>(src, TW, g, ws, b, x, lane);
+        }
+    }
+    // the VR x TW tile of d out
+    if ((TW & 3) == 0) {
+        const int TW4 = TW >> 2;
+        for (int q = threadIdx.x; q < VR * TW4; q += blockDim.x) {
+            const int r = q / TW4, c4 = q - r * TW4;
+            reinterpret_cast<float4*>(d + (int64_t)(a0 + r) * s + i0)[c4] = reinterpret_cast<const float4*>(sd)[q];
+        }
+    } else {
+        for (int q = threadIdx.x; q < VR * TW; q += blockDim.x) {
+            const int r = q / TW, c = q - r * TW;
+            d[(int64_t)(a0 + r) * s + i0 + c] = sd[q];
         }
     }
     __syncthreads();

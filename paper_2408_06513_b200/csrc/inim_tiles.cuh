@@ -44,7 +44,55 @@ INIM_DEV void store_row_cs(float* p, const float (&v)[CPL]) {
 //   urbot[b][c] (in-tile chains of the column prefix V at the
 //   band's last row), ule/ure[b][x][r] (chains at the tile's last / first column, complete
 //   in-band values since TW >= TH), rowsum[j][x].
-template <int CPL>
+// Exclusive prefix of a line of n values (one warp, float64, loads through L2 so other
+// warps' writes of this launch are seen); returns the line total.
+template <typename T>
+__device__ __forceinline__ double warp_line_prefix(const T* src, double* __restrict__ dst, int n, int lane) {
+    double carry = 0.0;
+    for (int base = 0; base < n; base += 32) {
+        const int x = base + lane;
+        const double v = x < n ? (double)__ldcg(src + x) : 0.0;
+        const double inc = warp_inclusive_scan_d(v, lane);
+        if (x < n) dst[x] = carry + inc - v;
+        carry += __shfl_sync(kFull, inc, 31);
+    }
+    return carry;
+}
+
+// The lines of band b (run by the warp that reduced the band's last tile): for each row
+// j the exclusive prefix over tiles of the row sums (HC[j][x]) and the in-band inclusive
+// prefix of the row totals (rpre); the exclusive prefix over tiles of the tile totals
+// (tilepre) and the band total (btot).  Lane q walks row q serially (its loads issued
+// 16 at a time), so the whole band costs a few memory round trips.
+__device__ __forceinline__ void band_lines_warp(const Geo& g, const Ws& ws, int b, int lane) {
+    const int TH = g.TH, NX = g.NX, a = b * TH;
+    const double bt = warp_line_prefix(ws.tiletot + (int64_t)b * NX, ws.tilepre + (int64_t)b * NX, NX, lane);
+    if (lane == 0) ws.btot[b] = bt;
+    double rt = 0.0;
+    if (lane < TH) {
+        const float* rs = ws.rowsum + (int64_t)(a + lane) * NX;
+        double* hc = ws.hc + (int64_t)(a + lane) * NX;
+        constexpr int U = 16;
+        for (int x0 = 0; x0 < NX; x0 += U) {
+            float v[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = x0 + q < NX ? __ldcg(rs + x0 + q) : 0.f;
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                if (x0 + q < NX) hc[x0 + q] = rt;
+                rt += (double)v[q];
+            }
+        }
+    }
+    const double inc = warp_inclusive_scan_d(rt, lane);
+    if (lane < TH) ws.rpre[a + lane] = inc;
+}
+
+// LINES: count the band's reduced tiles; the warp that completes the band runs
+// band_lines_warp (threadfence-reduction pattern: no warp waits on another).  The
+// counters start at zero (cleared by the kernel before the reduce, or by a memset) and
+// are reset by the last warp.
+template <int CPL, bool LINES = true>
 __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
                                                  int lane) {
     const int TH = g.TH, TW = g.TW, s = g.s, NX = g.NX;
@@ -113,6 +161,17 @@ __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const
         ws.ule[tile * TH + lane] = ule_mine;
         ws.ure[tile * TH + lane] = ure_mine;
         ws.rowsum[(int64_t)(a + lane) * NX + x] = rs_mine;
+    }
+    if (LINES) {
+        __threadfence();
+        unsigned old = 0;
+        if (lane == 0) old = atomicAdd(ws.bandctr + b, 1u);
+        old = __shfl_sync(kFull, old, 0);
+        if (old == (unsigned)(NX - 1)) {
+            __threadfence();
+            band_lines_warp(g, ws, b, lane);
+            if (lane == 0) ws.bandctr[b] = 0u;
+        }
     }
 }
 
@@ -230,23 +289,38 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
     const bool act = lane <= last;
     const int a = b * TH, i0 = x * TW;
     const int64_t tile = (int64_t)b * NX + x;
-    const double C = *ws.total;
+    const double* __restrict__ bandpre = ws.bandpre;
+    const double C = bandpre[B];
     const double invC = 1.0 / C;
     constexpr bool diff = MODE == 1;  // fold the flat response in
     const double inv_s = ldexp(1.0, -g.k), inv_s2 = inv_s * inv_s;
-    const double* __restrict__ tlc = ws.tlcar + (int64_t)b * s;
-    const double* __restrict__ cpre = ws.tlcar + (int64_t)B * s;
-    const double* __restrict__ x1 = ws.x1 + (int64_t)b * s;
-    const double* __restrict__ x2 = ws.x2 + (int64_t)b * (s + TH);
-    const double* __restrict__ apre = ws.apre;
-    const double* __restrict__ dsuf = ws.dsuf + (s - 1);  // index by delta = i - j
+    const float* __restrict__ tlc = ws.tlcar + (int64_t)b * s;
+    const float* __restrict__ cpre = ws.tlcar + (int64_t)B * s;
+    const float* __restrict__ x1 = ws.x1 + (int64_t)b * s;
+    const float* __restrict__ x2 = ws.x2 + (int64_t)b * (s + TH);
+    // diagonal marginals read off the chain carries (inim_scan.cuh "marg")
+    auto apre = [&](int sg) -> double {  // Apre[sigma]
+        if (sg < s) {
+            const int bb = sg / TH, r = sg - bb * TH;
+            return (double)ws.ure[(int64_t)bb * NX * TH + r] + (double)ws.x2[(int64_t)bb * (s + TH) + r + 1];
+        }
+        return (double)ws.x2[(int64_t)B * (s + TH) + sg - (s - 1)];
+    };
+    auto dsuf = [&](int dl) -> double {  // Dsuf[delta]
+        if (dl >= 0) {
+            const int j = s - 1 - dl, bb = j / TH, r = j - bb * TH, c2 = s - 2 - r;
+            return (double)ws.ule[((int64_t)bb * NX + NX - 1) * TH + r] + bandpre[bb] +
+                   (c2 >= 0 ? (double)ws.x1[(int64_t)bb * s + c2] : 0.0);
+        }
+        return (double)ws.x1[(int64_t)B * s + s - 1 + dl] + C;
+    };
     // normalised marginal entries (MODE 1): value / C, minus the flat value when folding
     auto nap = [&](int sg) {
-        const double v = apre[sg] * invC;
+        const double v = apre(sg) * invC;
         return (float)(diff ? v - (double)flat_apre_count(sg, s) * inv_s2 : v);
     };
     auto nds = [&](int dl) {
-        const double v = dsuf[dl] * invC;
+        const double v = dsuf(dl) * invC;
         return (float)(diff ? v - (double)flat_dsuf_count(dl, s) * inv_s2 : v);
     };
     // per-column constants and initial windows (row 0)
@@ -255,14 +329,14 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
     for (int e = 0; e < CPL; ++e) {
         const int i = i0 + u0 + e;
         const bool ok = act && i < s;
-        const double tv = ok ? tlc[i] : 0.0, cv = ok ? cpre[i] : 0.0;
+        const double tv = ok ? (double)tlc[i] : 0.0, cv = ok ? (double)cpre[i] : 0.0;
         A[e] = (float)tv;
         w1[e] = (float)(ok && i - 1 >= 0 ? x1[i - 1] : 0.0);  // X1[i - r - 1]
         w2[e] = (float)(ok ? x2[i + 1] : 0.0);                // X2[i + r + 1]
         if (MODE == 0) {
             Bc[e] = (float)(cv - tv);
-            wa[e] = (float)(ok ? apre[a + i] : 0.0);  // Apre[i + j]
-            wd[e] = (float)(ok ? dsuf[i - a] : 0.0);  // Dsuf[i - j]
+            wa[e] = (float)(ok ? apre(a + i) : 0.0);  // Apre[i + j]
+            wd[e] = (float)(ok ? dsuf(i - a) : 0.0);  // Dsuf[i - j]
         } else {
             Bc[e] = (float)(diff ? cv * invC - (i + 1) * inv_s : cv * invC);  // Cp
             wa[e] = ok ? nap(a + i) : 0.f;
@@ -277,7 +351,7 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         const double hc = lane < TH ? ws.hc[(int64_t)(a + lane) * NX + x] : 0.0;
         const double vh = warp_inclusive_scan_d(hc, lane);
         if (lane < TH) {
-            const double Rp = ws.rpre[a + lane];
+            const double Rp = bandpre[b] + ws.rpre[a + lane];
             P = (float)vh;
             if (MODE == 0) {
                 Q = (float)(Rp - vh);
@@ -289,8 +363,8 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                 const int c1 = i0 - 2 - lane;
                 e1 = (float)(c1 >= 0 ? x1[c1] : 0.0);
                 e2 = (float)x2[i0 + TW + 1 + lane];
-                ea = MODE == 0 ? (float)apre[a + i0 + TW + lane] : nap(a + i0 + TW + lane);
-                ed = MODE == 0 ? (float)dsuf[i0 - a - 1 - lane] : nds(i0 - a - 1 - lane);
+                ea = MODE == 0 ? (float)apre(a + i0 + TW + lane) : nap(a + i0 + TW + lane);
+                ed = MODE == 0 ? (float)dsuf(i0 - a - 1 - lane) : nds(i0 - a - 1 - lane);
             }
             ulel = x > 0 ? ws.ule[(tile - 1) * TH + lane] : 0.f;
             urer = x < NX - 1 ? ws.ure[(tile + 1) * TH + lane] : 0.f;

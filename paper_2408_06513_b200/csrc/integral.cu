@@ -49,6 +49,7 @@ template <int CPL>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const __grid_constant__ CUtensorMap map,
                                                                    const float* d, const Geo g, const Ws ws,
                                                                    int use_tma) {
+    pdl_enter();
     extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kWarpsPerCta + w;
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const __grid_
 template <int CPL, int MODE>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) write_kernel(const float* __restrict__ d, const Geo g,
                                                                   const Ws ws, const WriteOut out, const int* state) {
+    pdl_enter();
     if (state && state[0]) return;  // displacement stop already reached
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kWarpsPerCta + w;
@@ -179,7 +181,9 @@ static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const C
     const int use_tma = (map != nullptr && tma_ok(g)) ? 1 : 0;
     CUtensorMap dummy;
     memset(&dummy, 0, sizeof(dummy));
-    reduce_kernel<CPL><<<tile_ctas(g), kWarpsPerCta * 32, smem, st>>>(use_tma ? *map : dummy, d, g, ws, use_tma);
+    const CUtensorMap& tm = use_tma ? *map : dummy;
+    INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), smem, st, tm, d, g, ws,
+                             use_tma));
     prof_mark(st, "reduce");
     return (int)cudaGetLastError();
 }
@@ -195,7 +199,8 @@ int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const 
 template <int CPL, int MODE>
 static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const WriteOut& out, const int* state,
                             cudaStream_t st) {
-    write_kernel<CPL, MODE><<<tile_ctas(g), kWarpsPerCta * 32, 0, st>>>(d, g, ws, out, state);
+    INIM_CUDA_TRY(launch_pdl(write_kernel<CPL, MODE>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws,
+                             out, state));
     prof_mark(st, MODE == 0 ? "write_tables" : "write_field");
     return (int)cudaGetLastError();
 }

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
     const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
     const int nH = (s / A.h.TWH) * (s / A.h.RH), nHx = s / A.h.TWH;
     const int nV = g.NX * (s / A.v.VR);
-    const int nchain = chains_items(g), nmarg = marg_entries(g);
+    const int nchain = chains_items(g);
     double(*part)[33] = reinterpret_cast<double(*)[33]>(smem);
     double* bp = reinterpret_cast<double*>(smem) + kMegaWarps * 33;
     double* shs = bp + g.B + 1;
@@ -136,17 +136,13 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
         fence_proxy_async_global();  // d (generic-proxy stores) is read by TMA in the field phase
         grid.sync();
         stamp(t);
-        // ---- carry scan
-        for (int b = blockIdx.x; b < g.B; b += gridDim.x) lines_item(g, A.ws, b, shs);
-        grid.sync();
-        stamp(t);
+        // ---- carry scan (the band lines ran at the end of the reduce)
         band_prefix(g, A.ws, bp, shs);  // every CTA: X2 chains need it
-        if (blockIdx.x == 0)
+        if (blockIdx.x == 0) {
             for (int q = threadIdx.x; q <= g.B; q += blockDim.x) A.ws.bandpre[q] = bp[q];
+            if (threadIdx.x == 0) *A.ws.total = bp[g.B];
+        }
         for (int item = blockIdx.x; item < nchain; item += gridDim.x) chains_item(g, A.ws, item, part, bp);
-        grid.sync();
-        stamp(t);
-        for (int64_t q = gtid; q < nmarg; q += gstride) marg_entry(g, A.ws, (int)q);
         grid.sync();
         stamp(t);
         // ---- field: one warp per tile, tile staged by TMA into the warp's slot

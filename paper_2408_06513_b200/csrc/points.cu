@@ -24,6 +24,7 @@ __device__ __forceinline__ void splat_one(uint32_t* counts, int pix) {
 __global__ void __launch_bounds__(256) splat_f32_kernel(const float4* __restrict__ pts2, const float* __restrict__ pts,
                                                         int64_t n, int k, uint32_t* __restrict__ counts,
                                                         const int* state, float* zero0, float* zero1) {
+    pdl_enter();
     if (state && state[0]) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (zero0) *zero0 = 0.f;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
                                                          float4* __restrict__ out2, float* __restrict__ out, int64_t n,
                                                          int clip, float* max_disp, const int* state,
                                                          uint32_t* __restrict__ splat_next, float* zn0, float* zn1) {
+    pdl_enter();
     const bool stopped = state && state[0];
     const int s = 1 << k;
     // fused splat of the next iteration (its count buffer was cleared by this
@@ -321,8 +323,8 @@ static unsigned grid_for(int64_t work, int per_block) {
 int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st,
                      float* zero0, float* zero1) {
     const int64_t npair = n >> 1;
-    splat_f32_kernel<<<grid_for(npair > 0 ? npair : 1, 256), 256, 0, st>>>(reinterpret_cast<const float4*>(pts), pts, n,
-                                                                          k, counts, state, zero0, zero1);
+    INIM_CUDA_TRY(launch_pdl(splat_f32_kernel, dim3(grid_for(npair > 0 ? npair : 1, 256)), dim3(256), 0, st,
+                             reinterpret_cast<const float4*>(pts), pts, n, k, counts, state, zero0, zero1));
     prof_mark(st, "splat");
     return (int)cudaGetLastError();
 }
@@ -363,9 +365,9 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
                       const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1) {
     const int64_t npair = n >> 1;
     auto kern = pairs ? sample_f32_kernel<true> : sample_f32_kernel<false>;
-    kern<<<resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), 256, 0, st>>>(
-        tg, k, reinterpret_cast<const float4*>(in), in, reinterpret_cast<float4*>(out), out, n, clip, max_disp, state,
-        splat_next, zn0, zn1);
+    INIM_CUDA_TRY(launch_pdl(kern, dim3(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256)), dim3(256), 0,
+                             st, tg, k, reinterpret_cast<const float4*>(in), in, reinterpret_cast<float4*>(out), out, n,
+                             clip, max_disp, state, splat_next, zn0, zn1));
     prof_mark(st, "sample");
     return (int)cudaGetLastError();
 }

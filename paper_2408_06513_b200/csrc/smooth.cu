@@ -11,8 +11,11 @@ namespace inim {
 template <int R, typename T>
 __global__ void __launch_bounds__(256) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
-                                                       uint32_t* __restrict__ zero_next) {
+                                                       uint32_t* __restrict__ zero_next, uint32_t* ctr, int nctr) {
+    pdl_enter();
     if (state && state[0]) return;
+    if (ctr && blockIdx.x == 0 && blockIdx.y == 0)
+        for (int q = threadIdx.x; q < nctr; q += blockDim.x) ctr[q] = 0u;  // band counters of the reduce
     extern __shared__ __align__(16) float hsm[];
     smooth_h_tile<R, T>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
 }
@@ -21,6 +24,7 @@ template <int R>
 __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__ tmp, float* __restrict__ d,
                                                        const Geo g, const VGeo v, const Ws ws, const Taps taps,
                                                        float background, int emit, const int* state) {
+    pdl_enter();
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
     smooth_v_tile<R>(tmp, d, g, v, ws, taps, background, emit, blockIdx.x, blockIdx.y, vsm);
@@ -43,7 +47,7 @@ void make_taps(int kernel_size, Taps* taps) {
 
 template <int R, typename T>
 static int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, uint32_t* zero_next,
-                    cudaStream_t st) {
+                    uint32_t* ctr, int nctr, cudaStream_t st) {
     const HGeo h = make_hgeo(s);
     const size_t smem = h_smem_bytes(h, R);
     static bool attr = false;
@@ -52,7 +56,8 @@ static int launch_h(const T* in, float* out, int s, const Taps& taps, const int*
         attr = true;
     }
     dim3 grid(s / h.TWH, s / h.RH);
-    smooth_h_kernel<R, T><<<grid, h.NWH * 32, smem, st>>>(in, out, s, h, taps, state, zero_next);
+    INIM_CUDA_TRY(launch_pdl(smooth_h_kernel<R, T>, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state,
+                             zero_next, ctr, nctr));
     prof_mark(st, "smooth_h");
     return (int)cudaGetLastError();
 }
@@ -68,7 +73,8 @@ static int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, cons
         attr = true;
     }
     dim3 grid(g.NX, g.s / v.VR);
-    smooth_v_kernel<R><<<grid, v.VB * v.GT, smem, st>>>(tmp, d, g, v, ws, taps, bg, emit, state);
+    INIM_CUDA_TRY(launch_pdl(smooth_v_kernel<R>, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
+                             state));
     prof_mark(st, emit ? "smooth_v_reduce" : "smooth_v");
     return (int)cudaGetLastError();
 }
@@ -77,8 +83,11 @@ template <int KS>
 static int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
     constexpr int R = 3 * KS;
-    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st)
-                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st);
+    uint32_t* ctr = emit ? ws.bandctr : nullptr;
+    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next,
+                                            ctr, g.B, st)
+                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, ctr,
+                                         g.B, st);
     if (rc) return rc;
     return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st);
 }

@@ -14,7 +14,7 @@ from bench import four_cluster  # noqa: E402
 from paper_2408_06513_b200 import _device as D  # noqa: E402
 from paper_2408_06513_b200 import _lib  # noqa: E402
 
-NAMES = ["splat", "smooth_h", "smooth_v+reduce", "lines", "chains", "marg", "field", "move"]
+NAMES = ["splat", "smooth_h", "smooth_v+reduce+lines", "chains", "field", "move"]
 
 
 def main():
