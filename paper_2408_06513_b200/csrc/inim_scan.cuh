@@ -82,9 +82,9 @@ __host__ __device__ inline int chain_warps(const Geo& g) {
     return ny < 1 ? 1 : (ny > 16 ? 16 : ny);
 }
 
-// One chain: its band range [lo, hi] (bands whose value is stored or whose step term
-// is non-zero), the step terms and the stores.  Columns: TL c = kk; X1 c_b = kk -
-// (B - b) TH (moves right); X2 c_b = kk - b TH (moves left).
+// One chain: columns TL c = kk; X1 c_b = kk - (B - b) TH (moves right); X2 c_b = kk - b TH
+// (moves left).  Its step terms are non-zero exactly for bands b in [lo, hi) (the
+// column c_{b+1} is inside the grid) and its values are stored for b in [lo, hi].
 template <int KIND>
 struct Chain {
     const Geo& g;
@@ -97,13 +97,13 @@ struct Chain {
         if (KIND == 0) {
             lo = 0;
             hi = B;
-        } else if (KIND == 1) {  // col(b) in [0, s) for b in [e0, e1]; terms for b in [e0 - 1, e1 - 1]
+        } else if (KIND == 1) {  // col(b) in [0, s) for b in [e0, e1]
             const int kap = kk - B * TH;
             const int e0 = kap >= 0 ? 0 : (-kap + TH - 1) / TH;
             const int e1 = s - 1 - kap < 0 ? -1 : min(B, (s - 1 - kap) / TH);
             lo = max(0, e0 - 1);
             hi = e1;
-        } else {  // col(b) in [0, s) for b in [f0, f1]; the entry step / border store at f0 - 1
+        } else {  // col(b) in [0, s) for b in [f0, f1]; entry step / border store at f0 - 1
             const int f0 = kk <= s - 1 ? 0 : (kk - s + TH) / TH;
             const int f1 = min(B, kk / TH);
             lo = max(0, f0 - 1);
@@ -113,25 +113,28 @@ struct Chain {
     __device__ __forceinline__ int col(int b) const {
         return KIND == 0 ? kk : (KIND == 1 ? kk - (g.B - b) * g.TH : kk - b * g.TH);
     }
-    __device__ __forceinline__ double batl(int b, int c) const {
-        return ws.tilepre[(int64_t)b * g.NX + (c >> g.twlog)] + (double)ws.inpre[(int64_t)b * g.s + c];
-    }
-    // step b -> b + 1 (b < B)
+    // step b -> b + 1, b in [lo, hi): the column col(b + 1) is inside the grid
     __device__ __forceinline__ double term(int b) const {
-        const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX;
-        if (KIND == 0) return batl(b, kk);
+        const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX, tl = g.twlog;
+        const double* __restrict__ tilepre = ws.tilepre;
+        const float* __restrict__ inpre = ws.inpre;
+        if (KIND == 0) {
+            const int64_t q = (int64_t)b * s + kk;
+            return tilepre[b * NX + (kk >> tl)] + (double)__ldg(inpre + q);
+        }
         const int c = col(b + 1);
-        if (c < 0 || c >= s) return 0.0;
-        const int x = c >> g.twlog, u = c & (TW - 1);
+        const int x = c >> tl, u = c & (TW - 1);
+        const int64_t q = (int64_t)b * s + c;
         if (KIND == 1) {
-            double v = (double)ws.ulbot[(int64_t)b * s + c] - batl(b, c);
+            double v = (double)__ldg(ws.ulbot + q) - ((double)__ldg(inpre + q) + tilepre[b * NX + x]);
             const int rr = TH - 2 - u;  // row where the chain leaves the tile on the left
-            if (x > 0 && rr >= 0) v += (double)ws.ule[((int64_t)b * NX + x - 1) * TH + rr];
+            if (rr >= 0 && x > 0) v += (double)__ldg(ws.ule + ((b * NX + x - 1) * TH + rr));
             return v;
         }
-        double v = (double)ws.urbot[(int64_t)b * s + c] + (c > 0 ? batl(b, c - 1) : 0.0);
+        double v = (double)__ldg(ws.urbot + q);
+        if (c > 0) v += (double)__ldg(inpre + q - 1) + tilepre[b * NX + ((c - 1) >> tl)];
         const int rq = TH - 1 - (TW - u);
-        if (x < NX - 1 && rq >= 0) v += (double)ws.ure[((int64_t)b * NX + x + 1) * TH + rq];
+        if (rq >= 0 && x < NX - 1) v += (double)__ldg(ws.ure + ((b * NX + x + 1) * TH + rq));
         if (c + TH >= s) v += bp[b];  // the chain enters the grid: X2_b beyond the border
         return v;
     }
@@ -141,10 +144,9 @@ struct Chain {
         if (KIND == 0) {
             ws.tlcar[(int64_t)b * s + c] = (float)run;
         } else if (KIND == 1) {
-            if (c >= 0 && c < s) ws.x1[(int64_t)b * s + c] = (float)run;
+            if (c >= 0) ws.x1[(int64_t)b * s + c] = (float)run;
         } else {
-            if (c >= 0 && c < s) ws.x2[(int64_t)b * (s + TH) + c] = (float)run;
-            else if (c >= s && c < s + TH) ws.x2[(int64_t)b * (s + TH) + c] = (float)bp[b];
+            ws.x2[(int64_t)b * (s + TH) + c] = (float)(c < s ? run : bp[b]);  // c < s + TH always
         }
     }
 };
@@ -153,15 +155,14 @@ struct Chain {
 // sums, then the scan with stores.
 template <int KIND>
 __device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, double (*part)[33], const double* bp) {
-    const int B = g.B;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, NY = blockDim.x >> 5;
-    const bool live = kk < (KIND == 0 ? g.s : g.s + B * g.TH);
+    const bool live = kk < (KIND == 0 ? g.s : g.s + g.B * g.TH);
     const Chain<KIND> T(g, ws, bp, kk);
-    const int len = live && T.hi >= T.lo ? T.hi - T.lo + 1 : 0;  // bands lo..hi (hi may be B: store only)
+    const int len = live && T.hi >= T.lo ? T.hi - T.lo + 1 : 0;  // bands lo..hi
     const int CH = (len + NY - 1) / NY;
     const int b0 = T.lo + min(len, ty * CH), b1 = T.lo + min(len, ty * CH + CH);  // [b0, b1)
-    const int tb1 = min(b1, B);  // step terms exist for b < B
-    constexpr int U = 4;  // terms in flight per thread
+    const int tb1 = min(b1, T.hi);  // step terms for b < hi
+    constexpr int U = 4;            // terms in flight per thread
     double loc = 0.0;
     {
         int b = b0;
@@ -192,7 +193,7 @@ __device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, 
     }
     for (; b < b1; ++b) {
         T.emit(b, run);
-        if (b < B) run += T.term(b);
+        if (b < T.hi) run += T.term(b);
     }
 }
 

@@ -28,6 +28,30 @@ INIM_DEV void load_row(const float* __restrict__ p, float (&v)[CPL]) {
 }
 
 template <int CPL>
+INIM_DEV void load_row_g(const float* __restrict__ p, float (&v)[CPL]) {
+    if constexpr (CPL == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else if constexpr (CPL == 2) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = q.x; v[1] = q.y;
+    } else {
+        v[0] = __ldg(p);
+    }
+}
+
+template <int CPL>
+INIM_DEV void store_row(float* p, const float (&v)[CPL]) {
+    if constexpr (CPL == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (CPL == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    } else {
+        *p = v[0];
+    }
+}
+
+template <int CPL>
 INIM_DEV void store_row_cs(float* p, const float (&v)[CPL]) {
     if constexpr (CPL == 4) {
         __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
@@ -88,28 +112,31 @@ __device__ __forceinline__ void band_lines_warp(const Geo& g, const Ws& ws, int 
     if (lane < TH) ws.rpre[a + lane] = inc;
 }
 
-// LINES: count the band's reduced tiles; the warp that completes the band runs
-// band_lines_warp (threadfence-reduction pattern: no warp waits on another).  The
-// counters start at zero (cleared by the kernel before the reduce, or by a memset) and
-// are reset by the last warp.
-template <int CPL, bool LINES = true>
-__device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
-                                                 int lane) {
-    const int TH = g.TH, TW = g.TW, s = g.s, NX = g.NX;
-    const int last = g.WL - 1;
-    const int u0 = lane * CPL;
-    const bool act = lane <= last;
+// Per-tile aggregates of the reduce, fed one row at a time (lane l holds columns
+// CPL*l .. CPL*l + CPL - 1 of the row).  finish() writes inpre / tiletot / ulbot / urbot
+// / rowsum; with LINES it counts the band's reduced tiles and the warp that completes
+// the band runs band_lines_warp (threadfence-reduction pattern: no warp waits on
+// another).  The counters start at zero (cleared by the kernel before the reduce, or by
+// a memset) and are reset by the last warp.
+template <int CPL>
+struct TileReducer {
+    const Geo& g;
+    const Ws& ws;
+    int b, x, lane, last;
+    bool act;
+    float* ule_t;  // edge chains, stored row by row by the edge lanes
+    float* ure_t;
     float V[CPL], UL[CPL], UR[CPL];
+    float rs_mine;
+    __device__ __forceinline__ TileReducer(const Geo& g_, const Ws& ws_, int b_, int x_, int lane_)
+        : g(g_), ws(ws_), b(b_), x(x_), lane(lane_), last(g_.WL - 1), act(lane_ <= g_.WL - 1), rs_mine(0.f) {
+        const int64_t tile = (int64_t)b * g.NX + x;
+        ule_t = ws.ule + tile * g.TH;
+        ure_t = ws.ure + tile * g.TH;
 #pragma unroll
-    for (int e = 0; e < CPL; ++e) V[e] = UL[e] = UR[e] = 0.f;
-    float ule_mine = 0.f, ure_mine = 0.f, rs_mine = 0.f;
-    for (int r = 0; r < TH; ++r) {
-        float dv[CPL];
-        if (act) load_row<CPL>(src + (size_t)r * ld + u0, dv);
-        else {
-#pragma unroll
-            for (int e = 0; e < CPL; ++e) dv[e] = 0.f;
-        }
+        for (int e = 0; e < CPL; ++e) V[e] = UL[e] = UR[e] = 0.f;
+    }
+    __device__ __forceinline__ void row(int r, const float (&dv)[CPL]) {
         float rsum = 0.f;
 #pragma unroll
         for (int e = 0; e < CPL; ++e) {
@@ -127,52 +154,89 @@ __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const
         for (int e = 0; e < CPL - 1; ++e) UR[e] = V[e] + UR[e + 1];
         UR[CPL - 1] = V[CPL - 1] + fromR;
         rsum = warp_sum(rsum);
-        const float ulr = __shfl_sync(kFull, UL[CPL - 1], last);
-        const float url = __shfl_sync(kFull, UR[0], 0);
-        if (lane == r) {
-            ule_mine = ulr;
-            ure_mine = url;
-            rs_mine = rsum;
-        }
+        if (lane == r) rs_mine = rsum;
+        if (lane == last) ule_t[r] = UL[CPL - 1];
+        if (lane == 0) ure_t[r] = UR[0];
     }
-    const int a = b * TH, i0 = x * TW;
-    const int64_t tile = (int64_t)b * NX + x;
-    // in-tile inclusive row prefix of the column sums (float64 scan over the lanes) and
-    // the tile total
-    double lsum = 0.0;
+    template <bool LINES>
+    __device__ __forceinline__ void finish() {
+        const int TH = g.TH, TW = g.TW, s = g.s, NX = g.NX;
+        const int a = b * TH, i0 = x * TW, u0 = lane * CPL;
+        // in-tile inclusive row prefix of the column sums (float64 scan over the lanes)
+        // and the tile total
+        double lsum = 0.0;
 #pragma unroll
-    for (int e = 0; e < CPL; ++e) lsum += (double)V[e];
-    const double linc = warp_inclusive_scan_d(lsum, lane);
-    if (act) {
-        float* ip = ws.inpre + (int64_t)b * s + i0 + u0;
-        float* ub = ws.ulbot + (int64_t)b * s + i0 + u0;
-        float* rb = ws.urbot + (int64_t)b * s + i0 + u0;
-        double run = linc - lsum;
+        for (int e = 0; e < CPL; ++e) lsum += (double)V[e];
+        const double linc = warp_inclusive_scan_d(lsum, lane);
+        if (act) {
+            float* ip = ws.inpre + (int64_t)b * s + i0 + u0;
+            float* ub = ws.ulbot + (int64_t)b * s + i0 + u0;
+            float* rb = ws.urbot + (int64_t)b * s + i0 + u0;
+            double run = linc - lsum;
 #pragma unroll
-        for (int e = 0; e < CPL; ++e) {
-            run += (double)V[e];
-            ip[e] = (float)run;
-            ub[e] = UL[e];
-            rb[e] = UR[e];
+            for (int e = 0; e < CPL; ++e) {
+                run += (double)V[e];
+                ip[e] = (float)run;
+                ub[e] = UL[e];
+                rb[e] = UR[e];
+            }
         }
-    }
-    if (lane == 31) ws.tiletot[tile] = linc;
-    if (lane < TH) {
-        ws.ule[tile * TH + lane] = ule_mine;
-        ws.ure[tile * TH + lane] = ure_mine;
-        ws.rowsum[(int64_t)(a + lane) * NX + x] = rs_mine;
-    }
-    if (LINES) {
-        __threadfence();
-        unsigned old = 0;
-        if (lane == 0) old = atomicAdd(ws.bandctr + b, 1u);
-        old = __shfl_sync(kFull, old, 0);
-        if (old == (unsigned)(NX - 1)) {
+        if (lane == 31) ws.tiletot[(int64_t)b * NX + x] = linc;
+        if (lane < TH) ws.rowsum[(int64_t)(a + lane) * NX + x] = rs_mine;
+        if (LINES) {
             __threadfence();
-            band_lines_warp(g, ws, b, lane);
-            if (lane == 0) ws.bandctr[b] = 0u;
+            unsigned old = 0;
+            if (lane == 0) old = atomicAdd(ws.bandctr + b, 1u);
+            old = __shfl_sync(kFull, old, 0);
+            if (old == (unsigned)(NX - 1)) {
+                __threadfence();
+                band_lines_warp(g, ws, b, lane);
+                if (lane == 0) ws.bandctr[b] = 0u;
+            }
         }
     }
+};
+
+// The reduce of one tile from `src` (tile origin, row stride ld): a staged tile
+// (shared memory), or with GSRC global memory read through a ring of PF rows in flight
+// per lane, refilled as rows retire (PF = 8 measured slower than 2: registers).
+template <int CPL, bool LINES = true, bool GSRC = false>
+__device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
+                                                 int lane) {
+    const int TH = g.TH;
+    const int u0 = lane * CPL;
+    const bool act = lane <= g.WL - 1;
+    TileReducer<CPL> red(g, ws, b, x, lane);
+    constexpr int PF = GSRC ? 2 : 1;
+    float ring[PF][CPL];
+    if (GSRC) {
+#pragma unroll
+        for (int q = 0; q < PF; ++q) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) ring[q][e] = 0.f;
+            if (act && q < TH) load_row_g<CPL>(src + (size_t)q * ld + u0, ring[q]);
+        }
+    }
+    for (int r0 = 0; r0 < TH; r0 += PF) {  // PF rows per trip: the ring slot is a compile-time index
+#pragma unroll
+        for (int q = 0; q < PF; ++q) {
+            const int r = r0 + q;
+            if (r >= TH) break;
+            float dv[CPL];
+            if (GSRC) {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) dv[e] = ring[q][e];
+                if (act && r + PF < TH) load_row_g<CPL>(src + (size_t)(r + PF) * ld + u0, ring[q]);
+            } else if (act) {
+                load_row<CPL>(src + (size_t)r * ld + u0, dv);
+            } else {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) dv[e] = 0.f;
+            }
+            red.row(r, dv);
+        }
+    }
+    red.template finish<LINES>();
 }
 
 // --------------------------------------------------------- flat response / anchors
@@ -254,18 +318,6 @@ INIM_DEV int64_t flat_dsuf_count(int dl, int s) {  // #{i' - j' >= dl}
     return dl >= 0 ? (S - dl) * (S - dl + 1) / 2 : S * S - (S + dl - 1) * (S + dl) / 2;
 }
 
-template <int CPL>
-INIM_DEV void load_row_g(const float* __restrict__ p, float (&v)[CPL]) {
-    if constexpr (CPL == 4) {
-        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
-        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
-    } else if constexpr (CPL == 2) {
-        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
-        v[0] = q.x; v[1] = q.y;
-    } else {
-        v[0] = __ldg(p);
-    }
-}
 
 // MODE 0: stream the eight tables (float32 assembly from float64-rounded constants).
 // MODE 1 / 2: deformation field (build_field, mapping.py:194-204), with the raw map in the

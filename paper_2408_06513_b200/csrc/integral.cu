@@ -45,21 +45,17 @@ __host__ __device__ inline size_t tile_smem_bytes(const Geo& g) {
     return kWarpsPerCta * ((size_t)g.TH * g.TW * sizeof(float) + 16);
 }
 
+// The reduce reads its tile straight from global memory (rows prefetched two ahead in
+// registers), so residency is bounded by registers only.
 template <int CPL>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const __grid_constant__ CUtensorMap map,
-                                                                   const float* d, const Geo g, const Ws ws,
-                                                                   int use_tma) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* __restrict__ d, const Geo g,
+                                                                   const Ws ws) {
     pdl_enter();
-    extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kWarpsPerCta + w;
     if (tile >= g.B * g.NX) return;
     const int b = tile / g.NX, x = tile - b * g.NX;
-    float* slot = reinterpret_cast<float*>(smem) + (size_t)w * g.TH * g.TW;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kWarpsPerCta * (size_t)g.TH * g.TW * sizeof(float)) + w;
-    if (use_tma && lane == 0) prefetch_tensormap(&map);
-    warp_load_tile(slot, bar, &map, d, g, b, x, use_tma, lane);
-    warp_tile_reduce<CPL>(slot, g.TW, g, ws, b, x, lane);
+    warp_tile_reduce<CPL, true, true>(d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW, g.s, g, ws, b, x, lane);
 }
 
 // The write pass re-reads its tile straight from global memory (rows prefetched two
@@ -171,28 +167,17 @@ static bool tma_ok(const Geo& g) { return g.TW >= 32; }
 static unsigned tile_ctas(const Geo& g) { return (unsigned)((g.B * g.NX + kWarpsPerCta - 1) / kWarpsPerCta); }
 
 template <int CPL>
-static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, cudaStream_t st) {
-    const size_t smem = tile_smem_bytes(g);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(reduce_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    const int use_tma = (map != nullptr && tma_ok(g)) ? 1 : 0;
-    CUtensorMap dummy;
-    memset(&dummy, 0, sizeof(dummy));
-    const CUtensorMap& tm = use_tma ? *map : dummy;
-    INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), smem, st, tm, d, g, ws,
-                             use_tma));
+static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, cudaStream_t st) {
+    INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws));
     prof_mark(st, "reduce");
     return (int)cudaGetLastError();
 }
 
 int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, cudaStream_t st) {
     switch (g.CPL) {
-        case 4: return launch_reduce_cpl<4>(d, g, ws, map, st);
-        case 2: return launch_reduce_cpl<2>(d, g, ws, map, st);
-        default: return launch_reduce_cpl<1>(d, g, ws, map, st);
+        case 4: return launch_reduce_cpl<4>(d, g, ws, st);
+        case 2: return launch_reduce_cpl<2>(d, g, ws, st);
+        default: return launch_reduce_cpl<1>(d, g, ws, st);
     }
 }
 

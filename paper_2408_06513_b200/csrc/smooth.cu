@@ -65,6 +65,7 @@ static int launch_h(const T* in, float* out, int s, const Taps& taps, const int*
 template <int R>
 static int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, const Taps& taps, float bg, int emit,
                     const int* state, cudaStream_t st) {
+
     const VGeo v = make_vgeo(g);
     const size_t smem = v_smem_bytes(g, v, R);
     static bool attr = false;
