@@ -72,9 +72,15 @@ def to_device(a, dtype=torch.float32) -> torch.Tensor:
 def to_host64(t: torch.Tensor) -> np.ndarray:
     """Device tensor -> host float64 ndarray (widened on the device)."""
     if t.dtype == torch.float64:
-        return t.detach().cpu().numpy()
+        host = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+        host.copy_(t.detach())
+        return host.numpy()
     lib = require_cuda()
     t = t.contiguous()
     out = torch.empty(t.shape, dtype=torch.float64, device=t.device)
     _lib.check(lib.inim_cast_f32_to_f64(ptr(t), ptr(out), t.numel(), stream()), "cast")
-    return out.cpu().numpy()
+    # page-locked destination from torch's caching host allocator (reused across calls):
+    # the copy is one DMA instead of a staged pageable copy into fresh pages
+    host = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(out)
+    return host.numpy()

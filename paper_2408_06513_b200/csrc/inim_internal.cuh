@@ -6,6 +6,8 @@
 // TW >= TH (a chain ending in a tile's last column stays inside that tile).  See DESIGN.md "Integral pass" for the derivation of every carry.
 #pragma once
 
+#include <stdlib.h>
+
 #include "inim_common.cuh"
 
 namespace inim {
@@ -27,6 +29,17 @@ inline Geo make_geo(int k) {
     // one warp per tile: 64 columns (2 per lane) up to 2048^2 for more warps on small
     // grids, 128 columns (4 per lane, 16-byte accesses) above
     g.TW = g.s <= 2048 ? (g.s < 64 ? g.s : 64) : 128;
+    {  // geometry experiments: INIM_GEO_TH / INIM_GEO_TW override the large-grid choice
+        static int th = -1, tw = -1;
+        if (th < 0) {
+            const char* a = getenv("INIM_GEO_TH");
+            const char* b = getenv("INIM_GEO_TW");
+            th = a ? atoi(a) : 0;
+            tw = b ? atoi(b) : 0;
+        }
+        if (g.s > 2048 && th) g.TH = th;
+        if (g.s > 2048 && tw) g.TW = tw;
+    }
     g.CPL = g.TW >= 128 ? 4 : (g.TW >= 64 ? 2 : 1);
     g.B = g.s / g.TH;
     g.NX = g.s / g.TW;

@@ -21,21 +21,33 @@ import numpy as np
 from .errors import CoordinateOutOfRange, InvalidParams, LabelLengthMismatch, NonFiniteCoordinate, OutOfRangeLevel
 
 
-@dataclass(frozen=True)
 class ScatterDataset:
-    """Ordered 2-D samples in the unit square (model.py:27-41)."""
+    """Ordered 2-D samples in the unit square (model.py:27-41): positions, optional
+    labels, and ids (default 0..n-1, materialised on first access so that wrapping a
+    large array costs nothing).  Immutable, like the reference's frozen dataclass."""
 
-    positions: np.ndarray
-    labels: Optional[np.ndarray] = None
-    ids: np.ndarray = field(default=None)  # type: ignore[assignment]
+    __slots__ = ("positions", "labels", "_ids")
 
-    def __post_init__(self):
-        if self.ids is None:
-            object.__setattr__(self, "ids", np.arange(len(self.positions)))
+    def __init__(self, positions: np.ndarray, labels: Optional[np.ndarray] = None, ids: Optional[np.ndarray] = None):
+        object.__setattr__(self, "positions", positions)
+        object.__setattr__(self, "labels", labels)
+        object.__setattr__(self, "_ids", ids)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("ScatterDataset is immutable")
+
+    @property
+    def ids(self) -> np.ndarray:
+        if self._ids is None:
+            object.__setattr__(self, "_ids", np.arange(len(self.positions)))
+        return self._ids
 
     @property
     def n(self) -> int:
         return len(self.positions)
+
+    def __repr__(self) -> str:
+        return f"ScatterDataset(n={self.n}, labels={'yes' if self.labels is not None else 'no'})"
 
 
 class _DeviceBacked:

@@ -145,8 +145,12 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
     end_ev = torch.cuda.Event(enable_timing=True)
     while done < params.iterations:
         c = min(chunk, params.iterations - done)
+        # per-iteration frames only when the thinning policy keeps one inside the chunk;
+        # the chunk's last frame is the point buffer itself
+        frames_needed = keep is None or any((done + t) in keep for t in range(1, c))
+        frames = b["frames"] if frames_needed else None
         start_ev.record()
-        _lib.check(lib.inim_run(D.ptr(pts), n, k, params.kernel_size, bg, c, eps, D.ptr(b["frames"]),
+        _lib.check(lib.inim_run(D.ptr(pts), n, k, params.kernel_size, bg, c, eps, D.ptr(frames),
                                 D.ptr(b["fields"]), D.ptr(b["disp"]), D.ptr(b["excs"]), D.ptr(state),
                                 D.ptr(b["ws"]), stream), "run")
         end_ev.record()
@@ -166,7 +170,8 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
                 result.fields.append(DeformationField(k=k, max_excursion=float(excs[t]),
                                                       device_targets=b["fields"][t].clone()))
             if keep is None or it in keep:
-                result._record(it, b["frames"][t + 1, :n].clone())
+                src_frame = b["frames"][t + 1, :n] if frames is not None else pts
+                result._record(it, src_frame.clone())
             else:
                 result.iterations = it
         done += executed
