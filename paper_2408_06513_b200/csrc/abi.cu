@@ -301,7 +301,7 @@ int inim_integral_set(const float* d, int k, float* tables8, double* total, void
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (g.TW >= 32) {
-        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, g.TH);
+        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, 8);  // the reduce's TMA ring (8-row chunks)
         if (rc) return rc;
         mp = &map;
     }
@@ -337,7 +337,7 @@ int inim_field_from_density(const float* d, int k, const float* defect, float* t
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (g.TW >= 32) {
-        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, g.TH);
+        int rc = make_tensor_map_2d(&map, d, g.s, g.TW, 8);  // the reduce's TMA ring (8-row chunks)
         if (rc) return rc;
         mp = &map;
     }

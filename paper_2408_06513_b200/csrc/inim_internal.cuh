@@ -37,8 +37,8 @@ inline Geo make_geo(int k) {
             th = a ? atoi(a) : 0;
             tw = b ? atoi(b) : 0;
         }
-        if (g.s > 2048 && th) g.TH = th;
-        if (g.s > 2048 && tw) g.TW = tw;
+        if (g.s >= 64 && th) g.TH = th;
+        if (g.s >= 64 && tw) g.TW = tw;
     }
     g.CPL = g.TW >= 128 ? 4 : (g.TW >= 64 ? 2 : 1);
     g.B = g.s / g.TH;

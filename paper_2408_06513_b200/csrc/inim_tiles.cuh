@@ -207,7 +207,7 @@ __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const
     const int u0 = lane * CPL;
     const bool act = lane <= g.WL - 1;
     TileReducer<CPL> red(g, ws, b, x, lane);
-    constexpr int PF = GSRC ? 2 : 1;
+    constexpr int PF = GSRC ? (CPL <= 2 ? 16 : 2) : 1;
     float ring[PF][CPL];
     if (GSRC) {
 #pragma unroll
@@ -440,16 +440,19 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
 #pragma unroll
         for (int e = 0; e < CPL; ++e) dnext[e] = __ldg(defrow + e);
     }
-    float c0[CPL], c1[CPL];  // GSRC: rows r and r + 1 in flight
+    // GSRC: a ring of PF rows in flight per lane, refilled as rows retire; with two
+    // columns per lane (16-row tiles) the whole tile is requested up front
+    constexpr int PF = GSRC ? (CPL <= 2 ? 16 : 2) : 1;
+    float ring[PF][CPL];
     if (GSRC) {
 #pragma unroll
-        for (int e = 0; e < CPL; ++e) c0[e] = c1[e] = 0.f;
-        if (act) {
-            load_row_g<CPL>(src + u0, c0);
-            if (TH > 1) load_row_g<CPL>(src + (size_t)ld + u0, c1);
+        for (int q = 0; q < PF; ++q) {
+#pragma unroll
+            for (int e = 0; e < CPL; ++e) ring[q][e] = 0.f;
+            if (act && q < TH) load_row_g<CPL>(src + (size_t)q * ld + u0, ring[q]);
         }
     }
-    // one row of the sweep; GSRC: `cb` holds row r and is refilled with row r + 2
+    // one row of the sweep; GSRC: `cb` holds row r and is refilled with row r + PF
     auto step = [&](const int r, float (&cb)[CPL]) {
         float2 dcur[CPL];
         if (defrow) {
@@ -464,7 +467,7 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         if (GSRC) {
 #pragma unroll
             for (int e = 0; e < CPL; ++e) dv[e] = cb[e];
-            if (act && r + 2 < TH) load_row_g<CPL>(src + (size_t)(r + 2) * ld + u0, cb);
+            if (act && r + PF < TH) load_row_g<CPL>(src + (size_t)(r + PF) * ld + u0, cb);
         } else if (act) {
             load_row<CPL>(src + (size_t)r * ld + u0, dv);
         } else {
@@ -587,9 +590,10 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         slide_right<CPL>(w2, e2, r, lane, last);
         slide_right<CPL>(wa, ea, r, lane, last);
     };
-    for (int r = 0; r < TH; r += 2) {  // two rows per trip so each prefetch buffer is a fixed register set
-        step(r, c0);
-        if (r + 1 < TH) step(r + 1, c1);
+    for (int r0 = 0; r0 < TH; r0 += PF) {  // PF rows per trip: the ring slot is a compile-time index
+#pragma unroll
+        for (int q = 0; q < PF; ++q)
+            if (r0 + q < TH) step(r0 + q, ring[q]);
     }
     if (MODE != 0) {
         exc = warp_max(exc);

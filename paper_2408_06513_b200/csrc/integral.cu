@@ -20,29 +20,71 @@ namespace inim {
 
 constexpr int kWarpsPerCta = 4;
 
-// Stage one TH x TW tile into this warp's shared-memory slot.
-__device__ __forceinline__ void warp_load_tile(float* slot, uint64_t* bar, const CUtensorMap* map, const float* d,
-                                               const Geo& g, int b, int x, bool use_tma, int lane) {
-    if (use_tma) {
-        if (lane == 0) {
-            mbar_init(bar, 1);
-            fence_barrier_init();
-            mbar_arrive_expect_tx(bar, (uint32_t)(g.TH * g.TW * sizeof(float)));
-            tma_load_2d(slot, map, x * g.TW, b * g.TH, bar);
-        }
-        __syncwarp();
-        mbar_wait(bar, 0);
-    } else {
-        for (int q = lane; q < g.TH * g.TW; q += 32) {
-            const int r = q / g.TW, u = q - r * g.TW;
-            slot[q] = d[(int64_t)(b * g.TH + r) * g.s + x * g.TW + u];
-        }
-        __syncwarp();
-    }
+// Reduce with a TMA ring: each warp streams its tile through two shared-memory slots
+// of kChunk rows (cp.async.bulk.tensor.2d, one mbarrier per slot): the next chunk is
+// in flight while the current one is reduced, and 8 KB of shared memory per warp keeps
+// ~28 warps resident per SM.  Warps are independent (no CTA barrier).
+constexpr int kChunk = 8;
+
+__host__ __device__ inline size_t ring_smem_bytes(const Geo& g) {
+    return (size_t)kWarpsPerCta * (2 * kChunk * g.TW * sizeof(float) + 2 * sizeof(uint64_t));
 }
 
-__host__ __device__ inline size_t tile_smem_bytes(const Geo& g) {
-    return kWarpsPerCta * ((size_t)g.TH * g.TW * sizeof(float) + 16);
+template <int CPL>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_ring_kernel(const __grid_constant__ CUtensorMap map,
+                                                                        const Geo g, const Ws ws) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * kWarpsPerCta + w;
+    if (tile >= g.B * g.NX) return;  // the whole warp
+    const int b = tile / g.NX, x = tile - b * g.NX;
+    const int TW = g.TW, nch = g.TH / kChunk;
+    const uint32_t chunk_bytes = (uint32_t)(kChunk * TW * sizeof(float));
+    float* buf = reinterpret_cast<float*>(smem) + (size_t)w * 2 * kChunk * TW;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kWarpsPerCta * 2 * chunk_bytes) + 2 * w;
+    if (lane == 0) {
+        prefetch_tensormap(&map);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+        for (int c = 0; c < 2 && c < nch; ++c) {
+            mbar_arrive_expect_tx(&bar[c], chunk_bytes);
+            tma_load_2d(buf + (size_t)c * kChunk * TW, &map, x * TW, b * g.TH + c * kChunk, &bar[c]);
+        }
+    }
+    __syncwarp();
+    TileReducer<CPL> red(g, ws, b, x, lane);
+    const bool act = lane <= g.WL - 1;
+    uint32_t ph0 = 0, ph1 = 0;
+    for (int c = 0; c < nch; ++c) {
+        const int slot = c & 1;
+        if (slot == 0) {
+            mbar_wait(&bar[0], ph0);
+            ph0 ^= 1u;
+        } else {
+            mbar_wait(&bar[1], ph1);
+            ph1 ^= 1u;
+        }
+        const float* src = buf + (size_t)slot * kChunk * TW + lane * CPL;
+#pragma unroll
+        for (int q = 0; q < kChunk; ++q) {
+            float dv[CPL];
+            if (act) load_row<CPL>(src + q * TW, dv);
+            else {
+#pragma unroll
+                for (int e = 0; e < CPL; ++e) dv[e] = 0.f;
+            }
+            red.row(c * kChunk + q, dv);
+        }
+        __syncwarp();  // every lane is done with the slot before it is refilled
+        if (lane == 0 && c + 2 < nch) {
+            fence_proxy_async();
+            mbar_arrive_expect_tx(&bar[slot], chunk_bytes);
+            tma_load_2d(buf + (size_t)slot * kChunk * TW, &map, x * TW, b * g.TH + (c + 2) * kChunk, &bar[slot]);
+        }
+    }
+    red.template finish<true>();
 }
 
 // The reduce reads its tile straight from global memory (rows prefetched two ahead in
@@ -162,22 +204,33 @@ __global__ void line_scan_kernel(const float* __restrict__ in, float* __restrict
 // =====================================================================================
 // Host launchers
 // =====================================================================================
-static bool tma_ok(const Geo& g) { return g.TW >= 32; }
 
 static unsigned tile_ctas(const Geo& g) { return (unsigned)((g.B * g.NX + kWarpsPerCta - 1) / kWarpsPerCta); }
 
 template <int CPL>
-static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, cudaStream_t st) {
-    INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws));
+static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* ring_map,
+                             cudaStream_t st) {
+    if (ring_map && g.TH % kChunk == 0 && g.TW >= 32) {
+        const size_t smem = ring_smem_bytes(g);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(reduce_ring_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr = true;
+        }
+        INIM_CUDA_TRY(launch_pdl(reduce_ring_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), smem, st,
+                                 *ring_map, g, ws));
+    } else {
+        INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws));
+    }
     prof_mark(st, "reduce");
     return (int)cudaGetLastError();
 }
 
 int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, cudaStream_t st) {
     switch (g.CPL) {
-        case 4: return launch_reduce_cpl<4>(d, g, ws, st);
-        case 2: return launch_reduce_cpl<2>(d, g, ws, st);
-        default: return launch_reduce_cpl<1>(d, g, ws, st);
+        case 4: return launch_reduce_cpl<4>(d, g, ws, map, st);
+        case 2: return launch_reduce_cpl<2>(d, g, ws, map, st);
+        default: return launch_reduce_cpl<1>(d, g, ws, map, st);
     }
 }
 
