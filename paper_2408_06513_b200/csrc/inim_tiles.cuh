@@ -136,6 +136,9 @@ struct TileReducer {
 #pragma unroll
         for (int e = 0; e < CPL; ++e) V[e] = UL[e] = UR[e] = 0.f;
     }
+    // ROWSUM: reduce the row's sum over the warp here (else the caller supplies the row
+    // sums through set_rowsum)
+    template <bool ROWSUM = true>
     __device__ __forceinline__ void row(int r, const float (&dv)[CPL]) {
         float rsum = 0.f;
 #pragma unroll
@@ -153,10 +156,15 @@ struct TileReducer {
 #pragma unroll
         for (int e = 0; e < CPL - 1; ++e) UR[e] = V[e] + UR[e + 1];
         UR[CPL - 1] = V[CPL - 1] + fromR;
-        rsum = warp_sum(rsum);
-        if (lane == r) rs_mine = rsum;
+        if (ROWSUM) {
+            rsum = warp_sum(rsum);
+            if (lane == r) rs_mine = rsum;
+        }
         if (lane == last) ule_t[r] = UL[CPL - 1];
         if (lane == 0) ure_t[r] = UR[0];
+    }
+    __device__ __forceinline__ void set_rowsum(int r, float v) {
+        if (lane == r) rs_mine = v;
     }
     template <bool LINES>
     __device__ __forceinline__ void finish() {

@@ -36,55 +36,79 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_ring_kernel(const __
     pdl_enter();
     extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * kWarpsPerCta + w;
-    if (tile >= g.B * g.NX) return;  // the whole warp
-    const int b = tile / g.NX, x = tile - b * g.NX;
+    const int tiles = g.B * g.NX;
+    const int stride = gridDim.x * kWarpsPerCta;  // persistent warps: tiles t0, t0 + stride, ...
+    const int t0 = blockIdx.x * kWarpsPerCta + w;
+    if (t0 >= tiles) return;  // the whole warp
     const int TW = g.TW, nch = g.TH / kChunk;
+    const int mine = (tiles - t0 + stride - 1) / stride;
+    const int K = mine * nch;  // this warp's chunk sequence over its tiles
     const uint32_t chunk_bytes = (uint32_t)(kChunk * TW * sizeof(float));
     float* buf = reinterpret_cast<float*>(smem) + (size_t)w * 2 * kChunk * TW;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kWarpsPerCta * 2 * chunk_bytes) + 2 * w;
+    auto issue = [&](int kq) {  // lane 0: chunk kq of the sequence into slot kq & 1
+        const int tile = t0 + (kq / nch) * stride, c = kq % nch;
+        const int b = tile / g.NX, x = tile - b * g.NX;
+        mbar_arrive_expect_tx(&bar[kq & 1], chunk_bytes);
+        tma_load_2d(buf + (size_t)(kq & 1) * kChunk * TW, &map, x * TW, b * g.TH + c * kChunk, &bar[kq & 1]);
+    };
     if (lane == 0) {
         prefetch_tensormap(&map);
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         fence_barrier_init();
-        for (int c = 0; c < 2 && c < nch; ++c) {
-            mbar_arrive_expect_tx(&bar[c], chunk_bytes);
-            tma_load_2d(buf + (size_t)c * kChunk * TW, &map, x * TW, b * g.TH + c * kChunk, &bar[c]);
-        }
+        issue(0);
+        if (K > 1) issue(1);
     }
     __syncwarp();
-    TileReducer<CPL> red(g, ws, b, x, lane);
     const bool act = lane <= g.WL - 1;
     uint32_t ph0 = 0, ph1 = 0;
-    for (int c = 0; c < nch; ++c) {
-        const int slot = c & 1;
-        if (slot == 0) {
-            mbar_wait(&bar[0], ph0);
-            ph0 ^= 1u;
-        } else {
-            mbar_wait(&bar[1], ph1);
-            ph1 ^= 1u;
-        }
-        const float* src = buf + (size_t)slot * kChunk * TW + lane * CPL;
-#pragma unroll
-        for (int q = 0; q < kChunk; ++q) {
-            float dv[CPL];
-            if (act) load_row<CPL>(src + q * TW, dv);
-            else {
-#pragma unroll
-                for (int e = 0; e < CPL; ++e) dv[e] = 0.f;
+    // row sums of a chunk: lane group q (32 / kChunk lanes) sums row q of the slot
+    constexpr int LPR = 32 / kChunk;
+    const int rq = lane / LPR, rl = lane - rq * LPR;
+    int kq = 0;
+    for (int tile = t0; tile < tiles; tile += stride) {
+        const int b = tile / g.NX, x = tile - b * g.NX;
+        TileReducer<CPL> red(g, ws, b, x, lane);
+        for (int c = 0; c < nch; ++c, ++kq) {
+            const int slot = kq & 1;
+            if (slot == 0) {
+                mbar_wait(&bar[0], ph0);
+                ph0 ^= 1u;
+            } else {
+                mbar_wait(&bar[1], ph1);
+                ph1 ^= 1u;
             }
-            red.row(c * kChunk + q, dv);
+            const float* sl = buf + (size_t)slot * kChunk * TW;
+            {  // the chunk's kChunk row sums, one shuffle pair per chunk instead of a warp sum per row
+                float acc = 0.f;
+                for (int u = rl * 4; u < TW; u += LPR * 4) {
+                    const float4 v4 = *reinterpret_cast<const float4*>(sl + rq * TW + u);
+                    acc += (v4.x + v4.y) + (v4.z + v4.w);
+                }
+#pragma unroll
+                for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+#pragma unroll
+                for (int q = 0; q < kChunk; ++q) red.set_rowsum(c * kChunk + q, __shfl_sync(kFull, acc, q * LPR));
+            }
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+                float dv[CPL];
+                if (act) load_row<CPL>(sl + q * TW + lane * CPL, dv);
+                else {
+#pragma unroll
+                    for (int e = 0; e < CPL; ++e) dv[e] = 0.f;
+                }
+                red.template row<false>(c * kChunk + q, dv);
+            }
+            __syncwarp();  // every lane is done with the slot before it is refilled
+            if (lane == 0 && kq + 2 < K) {
+                fence_proxy_async();
+                issue(kq + 2);
+            }
         }
-        __syncwarp();  // every lane is done with the slot before it is refilled
-        if (lane == 0 && c + 2 < nch) {
-            fence_proxy_async();
-            mbar_arrive_expect_tx(&bar[slot], chunk_bytes);
-            tma_load_2d(buf + (size_t)slot * kChunk * TW, &map, x * TW, b * g.TH + (c + 2) * kChunk, &bar[slot]);
-        }
+        red.template finish<true>();
     }
-    red.template finish<true>();
 }
 
 // The reduce reads its tile straight from global memory (rows prefetched two ahead in
@@ -217,8 +241,20 @@ static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const C
             cudaFuncSetAttribute(reduce_ring_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             attr = true;
         }
-        INIM_CUDA_TRY(launch_pdl(reduce_ring_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), smem, st,
-                                 *ring_map, g, ws));
+        static int per_sm = 0;
+        if (!per_sm) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reduce_ring_kernel<CPL>, kWarpsPerCta * 32, smem);
+            if (per_sm < 1) per_sm = 1;
+        }
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        // one tile per warp: persistent warps (grid capped at residency, several tiles
+        // per warp through the same ring) measured 2x slower at 16384^2
+        const unsigned ctas = tile_ctas(g);
+        (void)sms;
+        INIM_CUDA_TRY(launch_pdl(reduce_ring_kernel<CPL>, dim3(ctas), dim3(kWarpsPerCta * 32), smem, st, *ring_map, g,
+                                 ws));
     } else {
         INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws));
     }
