@@ -136,15 +136,34 @@ class ClockSampler(threading.Thread):
 # Algorithmic bytes per launch of each kernel,
 # n points, m = s^2 pixels.
 def algorithmic_bytes(name: str, n: int, m: int) -> int:
+    """Minimal DRAM bytes per launch of each kernel of the iteration (n points, m pixels);
+    DESIGN.md section 4.  Grid-sized aggregates (1/TH of the grid) are left out."""
     table = {
         "splat": 8 * n + 4 * m,            # read fp32 (x,y); counts written once
-        "smooth_h": 4 * m + 4 * m,         # read counts, write the horizontal pass
+        "smooth_h": 4 * m + 4 * m + 4 * m,  # read counts, write the horizontal pass, clear the next counts
         "smooth_v_reduce": 4 * m + 4 * m,  # read the horizontal pass, write d
-        "write_field": 4 * m + 8 * m,      # read d, write the (s,s,2) field
-        "sample": 16 * n + 8 * m,          # read + write fp32 points, field gathered once
-        "memset_counts": 4 * m,
+        "write_field": 4 * m + 8 * m,      # read d, write the (s,s,2) field once
+        "sample": 16 * n + 8 * m + 4 * m,  # read + write fp32 points, field gathered once, next counts written once
+        "memset_counts": 8 * m,
     }
     return table.get(name, 0)
+
+
+# ncu kernel names -> the names inim_profile_run reports
+NCU_NAMES = {"sample_f32_kernel": "sample", "write_kernel": "write_field", "smooth_h_kernel": "smooth_h",
+             "smooth_v_kernel": "smooth_v_reduce", "chains_kernel": "chains", "splat_f32_kernel": "splat"}
+
+
+def ncu_traffic(workload: str):
+    """Per-launch DRAM bytes (read + write) of each kernel from the committed ncu launch
+    list of this workload (profiles/traffic_<workload>.json, tools/traffic_json.py), or {}."""
+    f = Path(__file__).resolve().parent / "profiles" / f"traffic_{workload}.json"
+    if not f.exists():
+        return {}
+    try:
+        return json.loads(f.read_text()).get("per_launch_bytes", {})
+    except ValueError:
+        return {}
 
 
 def dist_env():
@@ -282,7 +301,10 @@ def bench_ours(args):
         "e2e": e2e,
         "gpu_launches": int(args.steps * (ITERS * lib.inim_kernels_per_iteration(k) + 1)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": None,
+                     "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+                     "traffic": ncu_traffic("c3" if c3 else "c2").get(dom),
+                     "traffic_source": f"profiles/traffic_{'c3' if c3 else 'c2'}.json (ncu dram__bytes_read+write "
+                                       "per launch, cold cache)",
                      "algorithmic_bytes_per_launch": dom_bytes, "avg_launch_us": kernels[dom]["avg_us"],
                      "peak_source": peaks["source"],
                      "method": "per-launch CUDA events on the launch stream (eager replay of the timed step)"},

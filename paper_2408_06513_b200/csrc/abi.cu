@@ -15,7 +15,7 @@ int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const
 int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cudaStream_t st);
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
                       const int* state, cudaStream_t st, bool pairs = false, uint32_t* splat_next = nullptr,
-                      float* zn0 = nullptr, float* zn1 = nullptr);
+                      float* zn0 = nullptr, float* zn1 = nullptr, bool sorted = false);
 int launch_sample_f64(const float* tg, int k, const double* in, double* out, int64_t n, int clip, cudaStream_t st);
 int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_t st);
 int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st);
@@ -27,10 +27,10 @@ int launch_field_from_tables(const float* t8, int k, const double* total, const 
                              float* max_exc, cudaStream_t st);
 int launch_flat_response(int k, float* defect, cudaStream_t st);
 int launch_line_scan(const float* in, float* out, int s, int dj, int di, int exclusive, cudaStream_t st);
-int cell_count(int k);
-int launch_sort_points(const float* pts, int64_t n, int k, int* hist, int* rank, float* sorted, int* perm,
-                       cudaStream_t st);
-int launch_unpermute(const float* sorted, const int* perm, int64_t n, float* out, cudaStream_t st);
+size_t sort_bsum_words(int k);
+int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* counts, uint32_t* cursor,
+                       uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st);
+int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st);
 bool mega_supported(const Geo& g, int kernel_size);
 int launch_mega(const Geo& g, const Ws& ws, int kernel_size, float bg, float eps, int iters, float* pts, float* pong,
                 int64_t n, uint32_t* counts, float* d, float* targets, const float* defect, float* frames,
@@ -49,6 +49,18 @@ static bool use_mega(const Geo& g, int ks) {
     return env && !g_prof && mega_supported(g, ks);
 }
 static unsigned long long* g_stamps = nullptr;  // set by inim_run_stamped
+
+// Pixel-order sort of the points inside inim_run (INIM_SORT=0 disables).
+constexpr int64_t kSortMinPoints = 1 << 16;
+constexpr int kSortMinIters = 3;
+static bool sort_points_enabled() {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("INIM_SORT");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return env == 1;
+}
 
 bool pdl_enabled() {
     static int env = -1;
@@ -97,9 +109,9 @@ static FullLayout full_layout(const Geo& g, int64_t n) {
     const size_t nn = (size_t)(n > 0 ? n : 1);
     F.sortA = take(sizeof(float) * 2 * nn);  // points in cell order (ping)
     F.sortB = take(sizeof(float) * 2 * nn);  // (pong)
-    F.perm = take(sizeof(int) * nn);         // sorted slot -> input row
-    F.rank = take(sizeof(int) * nn);
-    F.hist = take(sizeof(int) * (size_t)cell_count(g.k));
+    F.perm = take(sizeof(uint32_t) * nn);    // input row -> sorted slot
+    F.rank = take(0);
+    F.hist = take(sizeof(uint32_t) * sort_bsum_words(g.k));  // block sums of the sort's scan
     F.bytes = o;
     return F;
 }
@@ -112,6 +124,7 @@ struct Chain {
     bool splatted;       // this iteration's counts were filled by the previous move
     bool splat_next;     // fuse the next iteration's splat into this move
     float *next_exc, *next_disp;
+    bool sorted;         // the points are in pixel order (aggregated splat atomics)
 };
 
 // One iteration.  `counts` must be zero on entry (or already filled, chain.splatted);
@@ -122,7 +135,7 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
                              float background, const float* defect, uint32_t* counts, uint32_t* counts_next, float* d,
                              float* targets, float* max_exc, float* disp, float stop_eps, int* state, const Ws& ws,
                              const CUtensorMap* map, cudaStream_t st, float* pairs = nullptr,
-                             const Chain& chain = Chain{false, false, nullptr, nullptr}) {
+                             const Chain& chain = Chain{false, false, nullptr, nullptr, false}) {
     const int* flag = stop_eps > 0.f ? state : nullptr;
     int rc = 0;
     if (!chain.splatted) {
@@ -137,9 +150,9 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
     if (rc) return rc;
     uint32_t* sn = chain.splat_next ? counts_next : nullptr;
     rc = pairs ? launch_sample_f32(pairs, g.k, pts_in, pts_out, n, 1, disp, flag, st, true, sn, chain.next_exc,
-                                   chain.next_disp)
+                                   chain.next_disp, chain.sorted)
                : launch_sample_f32(targets, g.k, pts_in, pts_out, n, 1, disp, flag, st, false, sn, chain.next_exc,
-                                   chain.next_disp);
+                                   chain.next_disp, chain.sorted);
     if (rc) return rc;
     if (flag) {
         INIM_CUDA_TRY(launch_pdl(iter_end_kernel, dim3(1), dim3(1), 0, st, (const float*)disp, stop_eps, state));
@@ -191,7 +204,6 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     float* sortA = reinterpret_cast<float*>(base + F.sortA);
     float* sortB = reinterpret_cast<float*>(base + F.sortB);
     int* perm = reinterpret_cast<int*>(base + F.perm);
-    int* rank = reinterpret_cast<int*>(base + F.rank);
     int* hist = reinterpret_cast<int*>(base + F.hist);
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
@@ -214,29 +226,36 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     if (key.n > 0 && use_mega(g, key.ks))  // the whole run in one persistent launch
         return launch_mega(g, w, key.ks, key.bg, key.eps, key.iters, pts, sortB, key.n, counts, d, tg_scratch, defect,
                            frames, fields, disp, excursions, scratch, state, g_stamps, st);
-    // Optional spatial pre-sort of the points (kSortPoints): a single counting sort by
-    // cell; off until its hot-cell atomics are privatised (it currently costs more than
-    // the gathers it saves).
-    constexpr bool kSortPoints = false;
-    if (kSortPoints && key.n > 0) {
-        int rc = launch_sort_points(pts, key.n, g.k, hist, rank, sortA, perm, st);
+    // Spatial order: for runs long enough to amortise it, the points are sorted by pixel
+    // once (from the counts of iteration 0's splat, which the run needs anyway), the
+    // moves then gather coalesced field rows and merge their splat atomics, and the
+    // final positions (and recorded frames) are scattered back through perm.
+    const bool sorted = sort_points_enabled() && key.n >= kSortMinPoints && key.iters >= kSortMinIters;
+    auto disp_at = [&](int t) { return disp ? disp + t : scratch + 2 * (t & 1); };
+    auto exc_at = [&](int t) { return excursions ? excursions + t : scratch + 2 * (t & 1) + 1; };
+    if (sorted) {
+        const int* flag = key.eps > 0.f ? state : nullptr;
+        int rc = launch_splat_f32(pts, key.n, g.k, counts, flag, st, exc_at(0), disp_at(0));
+        if (rc) return rc;
+        // the other count buffer is the sort's cursor; iteration 0's smoothing clears it
+        rc = launch_sort_points(pts, key.n, g.k, counts, counts + g.m, reinterpret_cast<uint32_t*>(hist), sortA,
+                                reinterpret_cast<uint32_t*>(perm), st);
         if (rc) return rc;
     }
-    // Point buffers: the first move reads the caller's array and the last one writes it
-    // back (no staging copies); in between the moves ping-pong through sortA / sortB.
+    // Point buffers: unsorted, the first move reads the caller's array and the last one
+    // writes it back (no staging copies); in between the moves ping-pong through
+    // sortA / sortB.
     float* bufs[2] = {sortB, sortA};
     auto pos_in = [&](int t) -> float* {
-        if (t == 0) return kSortPoints ? sortA : pts;
+        if (t == 0) return sorted ? sortA : pts;
         return bufs[t & 1];
     };
     auto pos_out = [&](int t) -> float* {
-        if (t == key.iters - 1 && !kSortPoints) return pts;
+        if (t == key.iters - 1 && !sorted) return pts;
         return bufs[(t + 1) & 1];
     };
     // per-iteration device scalars: recorded arrays, else two alternating scratch slots
     // (the move of iteration t clears iteration t+1's slot while t's is still live)
-    auto disp_at = [&](int t) { return disp ? disp + t : scratch + 2 * (t & 1); };
-    auto exc_at = [&](int t) { return excursions ? excursions + t : scratch + 2 * (t & 1) + 1; };
     for (int t = 0; t < key.iters; ++t) {
         float* src = pos_in(t);
         float* dst = pos_out(t);
@@ -244,18 +263,20 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         uint32_t* cur = counts + (size_t)(t & 1) * g.m;
         uint32_t* next = counts + (size_t)((t + 1) & 1) * g.m;
         const bool more = t + 1 < key.iters && key.n > 0;
-        const Chain chain{t > 0, more, more ? exc_at(t + 1) : nullptr, more ? disp_at(t + 1) : nullptr};
+        const Chain chain{t > 0 || sorted, more, more ? exc_at(t + 1) : nullptr, more ? disp_at(t + 1) : nullptr,
+                          sorted};
         int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, tg, exc_at(t),
                                    disp_at(t), key.eps, state, w, mp, st, tg_scratch, chain);
         if (rc) return rc;
         if (frames && key.n > 0) {
             float* fr = frames + (size_t)(t + 1) * 2 * key.n;
-            rc = kSortPoints ? launch_unpermute(dst, perm, key.n, fr, st)
-                             : (int)cudaMemcpyAsync(fr, dst, pbytes, cudaMemcpyDeviceToDevice, st);
+            rc = sorted ? launch_unpermute(dst, reinterpret_cast<const uint32_t*>(perm), key.n, fr, st)
+                        : (int)cudaMemcpyAsync(fr, dst, pbytes, cudaMemcpyDeviceToDevice, st);
             if (rc) return rc;
         }
     }
-    if (kSortPoints && key.n > 0 && key.iters > 0) return launch_unpermute(pos_out(key.iters - 1), perm, key.n, pts, st);
+    if (sorted && key.iters > 0)
+        return launch_unpermute(pos_out(key.iters - 1), reinterpret_cast<const uint32_t*>(perm), key.n, pts, st);
     return 0;
 }
 

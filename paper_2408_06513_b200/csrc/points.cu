@@ -81,7 +81,8 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
                                                          const float4* __restrict__ in2, const float* __restrict__ in,
                                                          float4* __restrict__ out2, float* __restrict__ out, int64_t n,
                                                          int clip, float* max_disp, const int* state,
-                                                         uint32_t* __restrict__ splat_next, float* zn0, float* zn1) {
+                                                         uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
+                                                         int agg) {
     pdl_enter();
     const bool stopped = state && state[0];
     const int s = 1 << k;
@@ -122,11 +123,27 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
         for (int u = 0; u < U; ++u)
             if (p0 + u * stride < npair) __stcs(out2 + p0 + u * stride, o[u]);
         if (splat_next && !stopped) {
+            if (agg) {  // points in pixel order: lanes sharing a pixel merge into one red.add
+                const unsigned am = __activemask();
+                const int lane = threadIdx.x & 31;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (p0 + u * stride < npair) {
-                    atomicAdd(splat_next + pixel_of(o[u].y, s) * s + pixel_of(o[u].x, s), 1u);
-                    atomicAdd(splat_next + pixel_of(o[u].w, s) * s + pixel_of(o[u].z, s), 1u);
+                for (int u = 0; u < U; ++u) {
+                    const bool ok = p0 + u * stride < npair;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int pix = ok ? pixel_of(h ? o[u].w : o[u].y, s) * s + pixel_of(h ? o[u].z : o[u].x, s)
+                                           : -1;
+                        const unsigned grp = __match_any_sync(am, pix);
+                        if (ok && lane == __ffs(grp) - 1) atomicAdd(splat_next + pix, (uint32_t)__popc(grp));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (p0 + u * stride < npair) {
+                        atomicAdd(splat_next + pixel_of(o[u].y, s) * s + pixel_of(o[u].x, s), 1u);
+                        atomicAdd(splat_next + pixel_of(o[u].w, s) * s + pixel_of(o[u].z, s), 1u);
+                    }
                 }
             }
         }
@@ -164,107 +181,160 @@ __global__ void __launch_bounds__(256) sample_f64_kernel(const float2* __restric
 }
 
 // ---------------------------------------------------------------- spatial point order
-// A counting sort of the points by cell (a 2^cs x 2^cs grid of cells, at most 64 per
-// side), done once per run: consecutive points (one warp) then fall in the same cell, so
-// the bilinear gathers hit L1 and the splat's atomics share addresses.  Both passes
-// privatise the histogram in shared memory (one CTA per contiguous chunk of points), so
-// hot cells of clustered data cost one global atomic per CTA, not one per point.  No
-// result depends on the order (integer counts, independent per-point moves); frames are
-// scattered back through `perm`.
-__host__ __device__ inline int cells_log2(int k) { return k < 6 ? k : 6; }
+// A counting sort of the points by pixel (row-major), once per run, from the counts the
+// run's first splat produced anyway:
+//   scan    offsets = exclusive prefix of the counts (three launches: block sums, one
+//           CTA over the block sums, block scans)
+//   place   slot = atomicAdd(offsets[pixel], 1) (warp-aggregated with __match_any_sync
+//           when lanes share a pixel); the point goes to sorted[slot], its row to
+//           perm[slot]
+// Consecutive points then share field rows (coalesced bilinear gathers) and count
+// words (aggregated atomics).  No result depends on the order (integer counts,
+// independent per-point moves); the final positions (and recorded frames) are
+// scattered back through perm.
+constexpr int kScanItems = 16;                     // counts per thread
+constexpr int kScanBlock = 256 * kScanItems;       // counts per block
 
-__device__ __forceinline__ int cell_of(float x, float y, int k) {
-    const int s = 1 << k;
-    const int cs = cells_log2(k);
-    const int sh = k - cs;
-    return (pixel_of(y, s) >> sh) * (1 << cs) + (pixel_of(x, s) >> sh);
-}
-
-// pass 1: per-CTA shared-memory histogram of its chunk, flushed with one atomic per bin
-__global__ void __launch_bounds__(256) cell_hist_kernel(const float2* __restrict__ pts, int64_t n, int k,
-                                                        int* __restrict__ hist, int ncells, int64_t chunk) {
-    extern __shared__ int cnt[];
-    for (int i = threadIdx.x; i < ncells; i += blockDim.x) cnt[i] = 0;
-    __syncthreads();
-    const int64_t p0 = (int64_t)blockIdx.x * chunk, p1 = min(n, p0 + chunk);
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-        const float2 v = pts[p];
-        atomicAdd(cnt + cell_of(v.x, v.y, k), 1);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < ncells; i += blockDim.x)
-        if (cnt[i]) atomicAdd(hist + i, cnt[i]);
-}
-
-// pass 2: the CTA reserves one contiguous block per bin (one atomic each), then places
-// its points with shared-memory cursors
-__global__ void __launch_bounds__(256) cell_place_kernel(const float2* __restrict__ pts, int64_t n, int k,
-                                                         int* __restrict__ cursor, int ncells, int64_t chunk,
-                                                         float2* __restrict__ sorted, int* __restrict__ perm) {
-    extern __shared__ int sm[];
-    int* cnt = sm;
-    int* base = sm + ncells;
-    for (int i = threadIdx.x; i < ncells; i += blockDim.x) cnt[i] = 0;
-    __syncthreads();
-    const int64_t p0 = (int64_t)blockIdx.x * chunk, p1 = min(n, p0 + chunk);
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-        const float2 v = pts[p];
-        atomicAdd(cnt + cell_of(v.x, v.y, k), 1);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < ncells; i += blockDim.x) {
-        base[i] = cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0;
-        cnt[i] = 0;
-    }
-    __syncthreads();
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
-        const float2 v = pts[p];
-        const int c = cell_of(v.x, v.y, k);
-        const int slot = base[c] + atomicAdd(cnt + c, 1);
-        sorted[slot] = v;
-        perm[slot] = (int)p;
-    }
-}
-
-// Exclusive scan of the cell histogram, one block (cells <= 65536 for k <= 12,
-// 1M for k = 14: loops over tiles).
-__global__ void __launch_bounds__(1024) cell_scan_kernel(int* __restrict__ hist, int ncells) {
-    __shared__ int sh[33];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int carry = 0;
-    for (int base = 0; base < ncells; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        const int v = i < ncells ? hist[i] : 0;
-        int inc = v;
+__global__ void __launch_bounds__(256) scan_block_sums_kernel(const uint32_t* __restrict__ counts, int64_t m,
+                                                              uint32_t* __restrict__ bsum) {
+    pdl_enter();
+    const int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(kFull, inc, o);
-            if (lane >= o) inc += t;
+    for (int q = 0; q < kScanItems; q += 4) {
+        if (base + q < m) {
+            const uint4 c = __ldg(reinterpret_cast<const uint4*>(counts + base + q));
+            v += c.x + c.y + c.z + c.w;
         }
-        if (lane == 31) sh[w] = inc;
+    }
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    __shared__ uint32_t ws[8];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int q = 0; q < 8; ++q) t += ws[q];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// one CTA: exclusive scan of the block sums in place
+__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ bsum, int nb) {
+    pdl_enter();
+    __shared__ uint32_t ws[33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t carry = 0;
+    for (int base = 0; base < nb; base += blockDim.x) {
+        const int q = base + threadIdx.x;
+        const uint32_t v = q < nb ? bsum[q] : 0u;
+        uint32_t inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += n;
+        }
+        if (lane == 31) ws[w] = inc;
         __syncthreads();
         if (w == 0) {
-            const int t = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
-            int ti = t;
-#pragma unroll
+            const uint32_t t = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0u;
+            uint32_t ti = t;
             for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(kFull, ti, o);
-                if (lane >= o) ti += u;
+                const uint32_t n = __shfl_up_sync(kFull, ti, o);
+                if (lane >= o) ti += n;
             }
-            sh[lane] = ti - t;
-            if (lane == 31) sh[32] = ti;
+            ws[lane] = ti - t;
+            if (lane == 31) ws[32] = ti;
         }
         __syncthreads();
-        if (i < ncells) hist[i] = carry + sh[w] + inc - v;
-        carry += sh[32];
+        if (q < nb) bsum[q] = carry + ws[w] + inc - v;
+        carry += ws[32];
         __syncthreads();
     }
 }
 
-__global__ void __launch_bounds__(256) unpermute_kernel(const float2* __restrict__ sorted, const int* __restrict__ perm,
-                                                        int64_t n, float2* __restrict__ out) {
-    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
-        out[perm[q]] = sorted[q];
+__global__ void __launch_bounds__(256) scan_blocks_kernel(const uint32_t* __restrict__ counts, int64_t m,
+                                                          const uint32_t* __restrict__ bsum,
+                                                          uint32_t* __restrict__ offsets) {
+    pdl_enter();
+    const int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
+    uint32_t c[kScanItems];
+    uint32_t v = 0;
+#pragma unroll
+    for (int q = 0; q < kScanItems; q += 4) {
+        uint4 u = make_uint4(0u, 0u, 0u, 0u);
+        if (base + q < m) u = __ldg(reinterpret_cast<const uint4*>(counts + base + q));
+        c[q] = u.x; c[q + 1] = u.y; c[q + 2] = u.z; c[q + 3] = u.w;
+        v += u.x + u.y + u.z + u.w;
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t n = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += n;
+    }
+    __shared__ uint32_t ws[8];
+    if (lane == 31) ws[w] = inc;
+    __syncthreads();
+    uint32_t run = bsum[blockIdx.x] + inc - v;
+    for (int q = 0; q < w; ++q) run += ws[q];
+#pragma unroll
+    for (int q = 0; q < kScanItems; q += 4) {
+        uint4 o;
+        o.x = run; run += c[q];
+        o.y = run; run += c[q + 1];
+        o.z = run; run += c[q + 2];
+        o.w = run; run += c[q + 3];
+        if (base + q < m) *reinterpret_cast<uint4*>(offsets + base + q) = o;
+    }
+}
+
+__global__ void __launch_bounds__(256) place_points_kernel(const float2* __restrict__ pts, int64_t n, int k,
+                                                           uint32_t* __restrict__ cursor, float2* __restrict__ sorted,
+                                                           uint32_t* __restrict__ rank) {
+    pdl_enter();
+    const int s = 1 << k;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t iters = (n + stride - 1) / stride;  // uniform trip count: whole warps in __match_any_sync
+    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t it = 0; it < iters; ++it, p += stride) {
+        const bool live = p < n;
+        float2 v = make_float2(0.f, 0.f);
+        int pix = -1;
+        if (live) {
+            v = __ldg(pts + p);
+            pix = pixel_of(v.y, s) * s + pixel_of(v.x, s);
+        }
+        const unsigned grp = __match_any_sync(kFull, pix);
+        const int leader = __ffs(grp) - 1;
+        uint32_t base = 0;
+        if (live && lane == leader) base = atomicAdd(cursor + pix, (uint32_t)__popc(grp));
+        base = __shfl_sync(kFull, base, leader);
+        if (live) {
+            const uint32_t slot = base + __popc(grp & ((1u << lane) - 1u));
+            sorted[slot] = v;
+            rank[p] = slot;  // coalesced: the way back is a gather
+        }
+    }
+}
+
+// out[p] = sorted[rank[p]]: coalesced rank reads and output writes, gathered reads.
+__global__ void __launch_bounds__(256) unpermute_kernel(const float2* __restrict__ sorted,
+                                                        const uint32_t* __restrict__ rank, int64_t n,
+                                                        float2* __restrict__ out) {
+    pdl_enter();
+    constexpr int U = 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += U * stride) {
+        uint32_t r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u] = p + u * stride < n ? __ldg(rank + p + u * stride) : 0u;
+        float2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = p + u * stride < n ? __ldg(sorted + r[u]) : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (p + u * stride < n) __stcs(out + p + u * stride, v[u]);
+    }
 }
 
 __global__ void cast_f64_f32_kernel(const double* __restrict__ in, float* __restrict__ out, int64_t count) {
@@ -329,29 +399,28 @@ int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const
     return (int)cudaGetLastError();
 }
 
-int cell_count(int k) { return 1 << (2 * cells_log2(k)); }
-
-// hist: cell_count(k) ints (zeroed here, then the cursors); perm: n ints; sorted: n
-// float2.  `rank` is unused (kept for the workspace layout).
-int launch_sort_points(const float* pts, int64_t n, int k, int* hist, int* rank, float* sorted, int* perm,
-                       cudaStream_t st) {
-    (void)rank;
-    const int nc = cell_count(k);
-    INIM_CUDA_TRY(cudaMemsetAsync(hist, 0, sizeof(int) * nc, st));
-    const int ctas = sm_count() * 2;
-    const int64_t chunk = (n + ctas - 1) / ctas;
-    const float2* p2 = reinterpret_cast<const float2*>(pts);
-    cell_hist_kernel<<<ctas, 256, sizeof(int) * nc, st>>>(p2, n, k, hist, nc, chunk);
-    cell_scan_kernel<<<1, 1024, 0, st>>>(hist, nc);
-    cell_place_kernel<<<ctas, 256, 2 * sizeof(int) * nc, st>>>(p2, n, k, hist, nc, chunk,
-                                                               reinterpret_cast<float2*>(sorted), perm);
+// Sort the points by pixel: `counts` are the points' per-pixel counts (the run's first
+// splat), `cursor` an m-word scratch (destroyed), bsum ceil(m / kScanBlock) words.
+int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* counts, uint32_t* cursor,
+                       uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st) {
+    const int64_t m = (int64_t)1 << (2 * k);
+    const unsigned nb = (unsigned)((m + kScanBlock - 1) / kScanBlock);
+    INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb), dim3(256), 0, st, counts, m, bsum));
+    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb));
+    INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb), dim3(256), 0, st, counts, m, (const uint32_t*)bsum,
+                             cursor));
+    INIM_CUDA_TRY(launch_pdl(place_points_kernel, dim3(grid_for(n > 0 ? n : 1, 256)), dim3(256), 0, st,
+                             reinterpret_cast<const float2*>(pts), n, k, cursor, reinterpret_cast<float2*>(sorted),
+                             rank));
     prof_mark(st, "sort_points");
     return (int)cudaGetLastError();
 }
 
-int launch_unpermute(const float* sorted, const int* perm, int64_t n, float* out, cudaStream_t st) {
-    unpermute_kernel<<<grid_for(n > 0 ? n : 1, 256), 256, 0, st>>>(reinterpret_cast<const float2*>(sorted), perm, n,
-                                                                    reinterpret_cast<float2*>(out));
+size_t sort_bsum_words(int k) { return (size_t)((((int64_t)1 << (2 * k)) + kScanBlock - 1) / kScanBlock); }
+
+int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st) {
+    INIM_CUDA_TRY(launch_pdl(unpermute_kernel, dim3(grid_for(n > 0 ? n : 1, 256)), dim3(256), 0, st,
+                             reinterpret_cast<const float2*>(sorted), rank, n, reinterpret_cast<float2*>(out)));
     prof_mark(st, "unpermute");
     return (int)cudaGetLastError();
 }
@@ -362,12 +431,13 @@ int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cuda
 }
 
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
-                      const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1) {
+                      const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1,
+                      bool sorted) {
     const int64_t npair = n >> 1;
     auto kern = pairs ? sample_f32_kernel<true> : sample_f32_kernel<false>;
     INIM_CUDA_TRY(launch_pdl(kern, dim3(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256)), dim3(256), 0,
                              st, tg, k, reinterpret_cast<const float4*>(in), in, reinterpret_cast<float4*>(out), out, n,
-                             clip, max_disp, state, splat_next, zn0, zn1));
+                             clip, max_disp, state, splat_next, zn0, zn1, sorted ? 1 : 0));
     prof_mark(st, "sample");
     return (int)cudaGetLastError();
 }
