@@ -4,6 +4,8 @@
 // CTA-wide barriers, so every thread of the CTA must call it.
 #pragma once
 
+#include <type_traits>
+
 #include "inim_taps.cuh"
 #include "inim_tiles.cuh"
 
@@ -83,42 +85,101 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
     // warps over rows, lanes over columns (coalesced, no index division); every load of
     // a pass is issued before any of its shared-memory stores (up to RPW x NPR loads in
     // flight per thread)
-    constexpr int RPW = 4;                    // rows per warp per pass
+    constexpr int RPW = std::is_same<T, float>::value ? 4 : 2;  // rows per warp per pass
     constexpr int NPR = (128 + 2 * R + 31) / 32;  // columns per lane per row (TWH <= 128)
+    constexpr int NP4 = (128 + 2 * R + 127) / 128;  // 16-byte groups per lane per row (interior tiles)
+    const bool vec = interior && (TWH & 3) == 0 && ((i0 - R) & 3) == 0 && (s & 3) == 0;
     for (int r0 = w; r0 < RH; r0 += RPW * nw) {
-        T v[RPW][NPR];
+        if (vec) {  // 16-byte loads of 4 consecutive columns, transposed into shared memory
+            uint4 v4[RPW][NP4];
 #pragma unroll
-        for (int q = 0; q < RPW; ++q) {
-            const int r = r0 + q * nw;
-            const T* row = in + (int64_t)(j0 + (r < RH ? r : 0)) * s;
+            for (int q = 0; q < RPW; ++q) {
+                const int r = r0 + q * nw;
+                const uint4* row4 = reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const uint32_t*>(in) + (int64_t)(j0 + (r < RH ? r : 0)) * s + i0 - R);
 #pragma unroll
-            for (int e = 0; e < NPR; ++e) {
-                const int c = lane + 32 * e;
-                if (r < RH && c < W) v[q][e] = __ldg(row + (interior ? i0 - R + c : reflect_index(i0 - R + c, s)));
+                for (int e = 0; e < NP4; ++e) {
+                    const int c4 = lane + 32 * e;
+                    if (r < RH && 4 * c4 < W) v4[q][e] = __ldg(row4 + c4);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int r = r0 + q * nw;
+#pragma unroll
+                for (int e = 0; e < NP4; ++e) {
+                    const int c = 4 * (lane + 32 * e);
+                    if (r < RH && c < W) {
+                        const uint4 u = v4[q][e];
+                        if (sizeof(T) == 4 && std::is_same<T, float>::value) {
+                            sh[c * ld + r] = __uint_as_float(u.x);
+                            sh[(c + 1) * ld + r] = __uint_as_float(u.y);
+                            sh[(c + 2) * ld + r] = __uint_as_float(u.z);
+                            sh[(c + 3) * ld + r] = __uint_as_float(u.w);
+                        } else {
+                            sh[c * ld + r] = (float)u.x;
+                            sh[(c + 1) * ld + r] = (float)u.y;
+                            sh[(c + 2) * ld + r] = (float)u.z;
+                            sh[(c + 3) * ld + r] = (float)u.w;
+                        }
+                    }
+                }
+            }
+        } else {
+            T v[RPW][NPR];
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int r = r0 + q * nw;
+                const T* row = in + (int64_t)(j0 + (r < RH ? r : 0)) * s;
+#pragma unroll
+                for (int e = 0; e < NPR; ++e) {
+                    const int c = lane + 32 * e;
+                    if (r < RH && c < W) v[q][e] = __ldg(row + (interior ? i0 - R + c : reflect_index(i0 - R + c, s)));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
+                const int r = r0 + q * nw;
+#pragma unroll
+                for (int e = 0; e < NPR; ++e) {
+                    const int c = lane + 32 * e;
+                    if (r < RH && c < W) sh[c * ld + r] = (float)v[q][e];
+                }
             }
         }
+        if (zero_next) {  // clear this tile's block of the next count buffer (16-byte stores)
 #pragma unroll
-        for (int q = 0; q < RPW; ++q) {
-            const int r = r0 + q * nw;
-#pragma unroll
-            for (int e = 0; e < NPR; ++e) {
-                const int c = lane + 32 * e;
-                if (r < RH && c < W) sh[c * ld + r] = (float)v[q][e];
+            for (int q = 0; q < RPW; ++q) {
+                const int r = r0 + q * nw;
+                if (r >= RH) break;
+                if ((TWH & 3) == 0) {
+                    uint4* z4 = reinterpret_cast<uint4*>(zero_next + (int64_t)(j0 + r) * s + i0);
+                    for (int c4 = lane; c4 < (TWH >> 2); c4 += 32) z4[c4] = make_uint4(0u, 0u, 0u, 0u);
+                } else {
+                    for (int c = lane; c < TWH; c += 32) zero_next[(int64_t)(j0 + r) * s + i0 + c] = 0u;
+                }
             }
-            if (zero_next && r < RH)
-                for (int c = lane; c < TWH; c += 32) zero_next[(int64_t)(j0 + r) * s + i0 + c] = 0u;
         }
     }
     __syncthreads();
     if (lane < RH && w < h.NWH) {
         const int c0 = w * h.CW;
-        fir_line<R, 8>(
+        fir_line<R, 16>(
             taps, h.CW, [&](int q) { return sh[(c0 + q) * ld + lane]; },
             [&](int p, float v) { so[lane * (TWH + 1) + c0 + p] = v; });
     }
     __syncthreads();
-    for (int r = w; r < RH; r += nw)
-        for (int c = lane; c < TWH; c += 32) out[(int64_t)(j0 + r) * s + i0 + c] = so[r * (TWH + 1) + c];
+    if ((TWH & 3) == 0) {  // 16-byte stores of the output tile
+        const int TW4 = TWH >> 2;
+        for (int q = threadIdx.x; q < RH * TW4; q += blockDim.x) {
+            const int r = q / TW4, c = 4 * (q - r * TW4);
+            const float* sr = so + r * (TWH + 1) + c;
+            *reinterpret_cast<float4*>(out + (int64_t)(j0 + r) * s + i0 + c) = make_float4(sr[0], sr[1], sr[2], sr[3]);
+        }
+    } else {
+        for (int r = w; r < RH; r += nw)
+            for (int c = lane; c < TWH; c += 32) out[(int64_t)(j0 + r) * s + i0 + c] = so[r * (TWH + 1) + c];
+    }
     __syncthreads();  // the tile's shared memory may be reused by the caller's next tile
 }
 

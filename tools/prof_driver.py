@@ -4,6 +4,7 @@
   python tools/prof_driver.py integral   # inim_integral_set at 4096^2 (and 16384^2 with --big)
 """
 
+import os
 import sys
 from pathlib import Path
 
@@ -15,6 +16,9 @@ import torch  # noqa: E402
 from bench import four_cluster  # noqa: E402
 from paper_2408_06513_b200 import _device as D  # noqa: E402
 from paper_2408_06513_b200 import _lib  # noqa: E402
+
+
+ITER = int(os.environ.get("PROF_ITERS", "2"))
 
 
 def main():
@@ -31,7 +35,7 @@ def main():
         pts = torch.from_numpy(host.astype(np.float32)).to(dev)
         ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev)
         for _ in range(2):
-            _lib.check(lib.inim_run_uncached(D.ptr(pts), n, k, 8, 0.0, 2, 0.0, None, None, None, None, None,
+            _lib.check(lib.inim_run_uncached(D.ptr(pts), n, k, 8, 0.0, ITER, 0.0, None, None, None, None, None,
                                              D.ptr(ws), D.stream()), "run")
     else:
         ks = [12] + ([14] if "--big" in sys.argv else [])
