@@ -181,6 +181,42 @@ int inim_profile_run(float* pts, int64_t n, int k, int kernel_size, float backgr
  * cached graph references). */
 void inim_clear_graph_cache(void);
 
+/* inim_run with per-frame layout metrics (regularize.py:55-59,71-75 -> metrics.py:147-168).
+ * frame_stats: device u64[iterations][3] (cleared by the call) receives, for frame t+1
+ *   (the positions after iteration t): {occupied pixels, sum over 4x4-pixel bins of
+ *   count^2, sum of counts}, from which binned_stddev (metrics.py:46-59) and
+ *   overplotting (metrics.py:62-71) follow exactly.
+ * orig_sub (optional, "full" mode): device (n_sub, 2) float64 = frame 0 at the rows
+ *   `pick` (device int64[n_sub], NULL = the first n_sub rows, i.e. all of them);
+ *   moved_sub: device scratch (n_sub, 2) float64; nb_stats: device u64[iterations][2]
+ *   (cleared by the call) = {trustworthiness penalty sum, preserved pair count} of frame
+ *   t+1 against frame 0 (metrics.py:74-144), 1 <= n_neighbors < n_sub. */
+int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
+                     float* frames, float* fields, float* disp, float* excursions, int* state, void* ws,
+                     cudaStream_t stream, unsigned long long* frame_stats, const double* orig_sub, const int64_t* pick,
+                     int64_t n_sub, int n_neighbors, double* moved_sub, unsigned long long* nb_stats);
+
+/* Occupancy statistics of a count grid (binned_stddev metrics.py:46-59, overplotting
+ * metrics.py:62-71): out3 (device u64[3], NOT cleared) += {occupied pixels, sum over the
+ * 4x4-pixel bins of count^2 (k >= 2; 0 otherwise), sum of counts}. */
+int inim_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t stream);
+
+/* out[q] = float64(pts[perm[rows[q]]]) for q < m (rows / perm NULL = identity):
+ * gathers the fixed-seed subsample of metrics.py:139-141, 164-166. */
+int inim_gather_points(const void* pts, int pts_is_f64, const int64_t* rows, const uint32_t* perm, int64_t m,
+                       double* out, cudaStream_t stream);
+
+/* trustworthiness (metrics.py:74-113) numerator: *out (device u64, NOT cleared) += sum
+ * over samples i and their n_neighbors nearest others j in `moved` (ties -> lower
+ * index) of max(0, rank_orig(i, j) - n_neighbors).  1 <= n_neighbors < n. */
+int inim_trust_penalty(const double* orig, const double* moved, int64_t n, int n_neighbors, unsigned long long* out,
+                       cudaStream_t stream);
+
+/* orthogonal_ordering (metrics.py:116-144) numerator: *out (device u64, NOT cleared) +=
+ * number of pairs i < j whose x-order and y-order signs agree between the layouts. */
+int inim_order_pairs(const double* orig, const double* moved, int64_t n, unsigned long long* out,
+                     cudaStream_t stream);
+
 /* Host-buffer end-to-end call (the FFI a C/ctypes caller of the reference would bind):
  * pts_host (n,2) float64 in, final positions float64 out (may alias), `iterations`
  * fixed iterations.  Allocates and frees its own device memory; synchronises. */

@@ -490,3 +490,103 @@ done:
     free(own_defect);
     return rc;
 }
+
+/* ================================================================ layout metrics
+ * metrics.py restated over integers (the quantities the reference reduces to floats
+ * at its last step).  The neighbour ranks are counted directly instead of through the
+ * reference's full argsort: rank_i(j) = 1 + #{l != i : (d(i,l), l) < (d(i,j), j)},
+ * which is the position of j in a stable argsort of row i with self first
+ * (metrics.py:77-90).
+ */
+
+/* binned_stddev / overplotting moments (metrics.py:46-71) of a float64 layout:
+ * out[0] = occupied pixels, out[1] = sum over 4x4 bins of count^2 (k >= 2, else 0),
+ * out[2] = n. */
+int orc_frame_stats(const double* pos, int64_t n, int k, int64_t* out) {
+    if (k < 0 || k > 14 || n < 0 || !out) return 1;
+    const int64_t s = (int64_t)1 << k;
+    int64_t* cnt = (int64_t*)calloc((size_t)(s * s), sizeof(int64_t));
+    if (!cnt) return 2;
+    for (int64_t q = 0; q < n; ++q) cnt[pixel_index(pos[2 * q + 1], s) * s + pixel_index(pos[2 * q], s)] += 1;
+    int64_t occ = 0, sq = 0;
+    for (int64_t p = 0; p < s * s; ++p) occ += cnt[p] != 0;
+    if (k >= 2) {
+        const int64_t b = s / 4;
+        for (int64_t bj = 0; bj < b; ++bj)
+            for (int64_t bi = 0; bi < b; ++bi) {
+                int64_t c = 0;
+                for (int r = 0; r < 4; ++r)
+                    for (int q = 0; q < 4; ++q) c += cnt[(4 * bj + r) * s + 4 * bi + q];
+                sq += c * c;
+            }
+    }
+    free(cnt);
+    out[0] = occ;
+    out[1] = sq;
+    out[2] = n;
+    return 0;
+}
+
+static inline double orc_dist2(const double* p, int64_t i, int64_t j) {
+    const double dx = p[2 * i] - p[2 * j];
+    const double dy = p[2 * i + 1] - p[2 * j + 1];
+    return dx * dx + dy * dy; /* -ffp-contract=off: (dx*dx) + (dy*dy), two roundings */
+}
+
+static inline int key_before(double d, int64_t j, double e, int64_t l) { return d < e || (d == e && j < l); }
+
+/* trustworthiness numerator (metrics.py:95-108): sum over i of
+ * max(0, rank_orig_i(j) - nn) for the nn nearest j != i of the deformed layout. */
+int orc_trust_penalty(const double* orig, const double* moved, int64_t n, int nn, int64_t* out) {
+    if (n < 0 || nn < 1 || nn >= n || !out) return 1;
+    int64_t total = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : total)
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t sel[64];
+        int64_t* selp = nn <= 64 ? sel : (int64_t*)malloc(sizeof(int64_t) * (size_t)nn);
+        double last_d = -1.0;
+        int64_t last_j = -1;
+        for (int r = 0; r < nn; ++r) { /* r-th nearest by (distance, index) */
+            double bd = INFINITY;
+            int64_t bj = INT64_MAX;
+            for (int64_t j = 0; j < n; ++j) {
+                if (j == i) continue;
+                const double d = orc_dist2(moved, i, j);
+                if (key_before(last_d, last_j, d, j) && key_before(d, j, bd, bj)) {
+                    bd = d;
+                    bj = j;
+                }
+            }
+            selp[r] = bj;
+            last_d = bd;
+            last_j = bj;
+        }
+        for (int r = 0; r < nn; ++r) {
+            const int64_t j = selp[r];
+            const double dj = orc_dist2(orig, i, j);
+            int64_t rank = 1;
+            for (int64_t l = 0; l < n; ++l)
+                if (l != i && key_before(orc_dist2(orig, i, l), l, dj, j)) ++rank;
+            if (rank > nn) total += rank - nn;
+        }
+        if (selp != sel) free(selp);
+    }
+    *out = total;
+    return 0;
+}
+
+/* orthogonal_ordering numerator (metrics.py:136-143): pairs i < j whose x-order and
+ * y-order signs agree between the two layouts. */
+static inline int sgn3(double a, double b) { return (a > b) - (a < b); }
+
+int orc_order_pairs(const double* orig, const double* moved, int64_t n, int64_t* out) {
+    if (n < 0 || !out) return 1;
+    int64_t kept = 0;
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : kept)
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = i + 1; j < n; ++j)
+            kept += sgn3(orig[2 * i], orig[2 * j]) == sgn3(moved[2 * i], moved[2 * j]) &&
+                    sgn3(orig[2 * i + 1], orig[2 * j + 1]) == sgn3(moved[2 * i + 1], moved[2 * j + 1]);
+    *out = kept;
+    return 0;
+}

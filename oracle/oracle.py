@@ -229,3 +229,110 @@ def total(values) -> float:
     """float(values.sum()) restated with numpy's pairwise summation (integral.py:246)."""
     v = _f64(values).ravel()
     return lib().orc_sum(_p(v), len(v))
+
+
+# ------------------------------------------------------------------ layout metrics
+_SUBSAMPLE_CAP = 4096
+_SUBSAMPLE_SEED = 1789
+
+
+def _i64p(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+
+def _metric_lib():
+    L = lib()
+    if not getattr(L, "_metrics_typed", False):
+        ip = ctypes.POINTER(ctypes.c_int64)
+        L.orc_frame_stats.argtypes = [_dp, _i64, ctypes.c_int, ip]
+        L.orc_trust_penalty.argtypes = [_dp, _dp, _i64, ctypes.c_int, ip]
+        L.orc_order_pairs.argtypes = [_dp, _dp, _i64, ip]
+        L._metrics_typed = True
+    return L
+
+
+def frame_stats(positions, k: int):
+    """(occupied pixels, sum of squared 4x4-bin counts, n) (metrics.py:46-71)."""
+    pos = _f64(positions).reshape(-1, 2)
+    out = np.zeros(3, dtype=np.int64)
+    _check(_metric_lib().orc_frame_stats(_p(pos), len(pos), k, _i64p(out)), "frame_stats")
+    return tuple(int(v) for v in out)
+
+
+def binned_stddev(positions, k: int) -> float:
+    """metrics.binned_stddev (metrics.py:46-59): population std of the 4x4-bin counts,
+    from their exact integer moments (var = (B sum c^2 - n^2) / B^2, correctly rounded)."""
+    if k < 2:
+        raise ValueError("k must be >= 2 so 4x4-pixel bins tile the grid")
+    if len(positions) == 0:
+        return 0.0
+    _occ, sq, n = frame_stats(positions, k)
+    nb = ((1 << k) // 4) ** 2
+    return float(np.sqrt((nb * sq - n * n) / (nb * nb)))
+
+
+def overplotting(positions, k: int) -> float:
+    """metrics.overplotting (metrics.py:62-71)."""
+    n = len(positions)
+    if n == 0:
+        raise ValueError("overplotting needs at least one sample")
+    occ, _sq, _n = frame_stats(positions, k)
+    return (n - occ) / n
+
+
+def trust_penalty(original, deformed, n_neighbors: int = 10) -> int:
+    o, m = _f64(original).reshape(-1, 2), _f64(deformed).reshape(-1, 2)
+    out = np.zeros(1, dtype=np.int64)
+    _check(_metric_lib().orc_trust_penalty(_p(o), _p(m), len(o), int(n_neighbors), _i64p(out)), "trust")
+    return int(out[0])
+
+
+def trustworthiness(original, deformed, n_neighbors: int = 10) -> float:
+    """metrics.trustworthiness (metrics.py:74-113)."""
+    n = len(original)
+    if len(deformed) != n:
+        raise ValueError("arrays must have the same length")
+    if n <= n_neighbors:
+        raise ValueError(f"need more than {n_neighbors} samples")
+    total = float(trust_penalty(original, deformed, n_neighbors))
+    if total == 0.0:
+        return 1.0
+    return 1.0 - total / (n * n_neighbors * (2 * n - 3 * n_neighbors - 1) / 2.0)
+
+
+def subsample(n: int, cap: int = _SUBSAMPLE_CAP):
+    """The fixed-seed pick of metrics.py:132-134 / 162-165 (None if n <= cap)."""
+    if n <= cap:
+        return None
+    return np.random.Generator(np.random.PCG64(_SUBSAMPLE_SEED)).choice(n, size=cap, replace=False)
+
+
+def orthogonal_ordering(original, deformed, sample_cap: int = _SUBSAMPLE_CAP) -> float:
+    """metrics.orthogonal_ordering (metrics.py:116-144)."""
+    o, m = _f64(original).reshape(-1, 2), _f64(deformed).reshape(-1, 2)
+    n = len(o)
+    if len(m) != n:
+        raise ValueError("arrays must have the same length")
+    if n < 2:
+        return 1.0
+    pick = subsample(n, sample_cap)
+    if pick is not None:
+        o, m, n = np.ascontiguousarray(o[pick]), np.ascontiguousarray(m[pick]), sample_cap
+    out = np.zeros(1, dtype=np.int64)
+    _check(_metric_lib().orc_order_pairs(_p(o), _p(m), n, _i64p(out)), "order")
+    return int(out[0]) / (n * (n - 1) / 2)
+
+
+def record_for_frame(original, positions, k: int, full: bool = False, n_neighbors: int = 10):
+    """metrics.record_for_frame (metrics.py:147-168) -> (binned_stddev, overplotting,
+    trustworthiness | None, ordering | None)."""
+    trust = order = None
+    o, m = _f64(original).reshape(-1, 2), _f64(positions).reshape(-1, 2)
+    if full and len(m) > n_neighbors:
+        pick = subsample(len(o))
+        if pick is not None:
+            o, m = np.ascontiguousarray(o[pick]), np.ascontiguousarray(m[pick])
+        trust = trustworthiness(o, m, n_neighbors)
+        order = orthogonal_ordering(o, m)
+    pos = _f64(positions).reshape(-1, 2)
+    return (binned_stddev(pos, k), overplotting(pos, k) if len(pos) else 0.0, trust, order)

@@ -60,6 +60,13 @@ _SIGS = {
                                  ctypes.c_char_p, c_int]),
     "inim_run_host": (c_int, [c_void_p, c_void_p, c_i64, c_int, c_int, c_double, c_int]),
     "inim_kernels_per_iteration": (c_int, [c_int]),
+    "inim_run_metrics": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_float, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_i64, c_int,
+                                 c_void_p, c_void_p]),
+    "inim_frame_stats": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "inim_gather_points": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "inim_trust_penalty": (c_int, [c_void_p, c_void_p, c_i64, c_int, c_void_p, c_void_p]),
+    "inim_order_pairs": (c_int, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
 }
 
 INIM_EINVAL, INIM_ENOTPOW2, INIM_EKERNEL, INIM_EDRIVER = -1, -2, -3, -4

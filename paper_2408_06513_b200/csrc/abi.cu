@@ -31,6 +31,12 @@ size_t sort_bsum_words(int k);
 int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* counts, uint32_t* cursor,
                        uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st);
 int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st);
+int launch_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t st);
+int launch_gather_points(const void* pts, int is_f64, const int64_t* rows, const uint32_t* perm, int64_t m,
+                         double* out, cudaStream_t st);
+int launch_trust(const double* orig, const double* moved, int64_t n, int nn, unsigned long long* out,
+                 cudaStream_t st);
+int launch_order_pairs(const double* orig, const double* moved, int64_t n, unsigned long long* out, cudaStream_t st);
 bool mega_supported(const Geo& g, int kernel_size);
 int launch_mega(const Geo& g, const Ws& ws, int kernel_size, float bg, float eps, int iters, float* pts, float* pong,
                 int64_t n, uint32_t* counts, float* d, float* targets, const float* defect, float* frames,
@@ -179,6 +185,10 @@ struct RunKey {
     float eps;
     const void *frames, *fields, *disp, *exc, *state, *ws;
     cudaStream_t st;
+    // per-frame metrics (regularize.py:55-59,71-75); all null = none
+    const void *fstats, *orig_sub, *pick, *moved_sub, *nbstats;
+    int64_t n_sub;
+    int n_neighbors;
     bool operator==(const RunKey& o) const { return memcmp(this, &o, sizeof(RunKey)) == 0; }
 };
 
@@ -223,7 +233,15 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     }
     const size_t pbytes = sizeof(float) * 2 * (size_t)key.n;
     if (frames && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(frames, pts, pbytes, cudaMemcpyDeviceToDevice, st));
-    if (key.n > 0 && use_mega(g, key.ks))  // the whole run in one persistent launch
+    // Per-frame metrics: occupancy statistics of frame t+1 come off the counts the move
+    // of iteration t splats (so the last move splats too); neighbourhood metrics of the
+    // fixed subsample against frame 0.
+    unsigned long long* fstats = (unsigned long long*)key.fstats;
+    unsigned long long* nbstats = (unsigned long long*)key.nbstats;
+    const bool nb = fstats && key.orig_sub && nbstats && key.moved_sub && key.n_sub > 0;
+    if (fstats) INIM_CUDA_TRY(cudaMemsetAsync(fstats, 0, sizeof(unsigned long long) * 3 * key.iters, st));
+    if (nb) INIM_CUDA_TRY(cudaMemsetAsync(nbstats, 0, sizeof(unsigned long long) * 2 * key.iters, st));
+    if (key.n > 0 && !fstats && use_mega(g, key.ks))  // the whole run in one persistent launch
         return launch_mega(g, w, key.ks, key.bg, key.eps, key.iters, pts, sortB, key.n, counts, d, tg_scratch, defect,
                            frames, fields, disp, excursions, scratch, state, g_stamps, st);
     // Spatial order: for runs long enough to amortise it, the points are sorted by pixel
@@ -263,8 +281,9 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         uint32_t* cur = counts + (size_t)(t & 1) * g.m;
         uint32_t* next = counts + (size_t)((t + 1) & 1) * g.m;
         const bool more = t + 1 < key.iters && key.n > 0;
-        const Chain chain{t > 0 || sorted, more, more ? exc_at(t + 1) : nullptr, more ? disp_at(t + 1) : nullptr,
-                          sorted};
+        const bool splat_next = more || (fstats && key.n > 0);
+        const Chain chain{t > 0 || sorted, splat_next, more ? exc_at(t + 1) : nullptr,
+                          more ? disp_at(t + 1) : nullptr, sorted};
         int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, tg, exc_at(t),
                                    disp_at(t), key.eps, state, w, mp, st, tg_scratch, chain);
         if (rc) return rc;
@@ -272,6 +291,18 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
             float* fr = frames + (size_t)(t + 1) * 2 * key.n;
             rc = sorted ? launch_unpermute(dst, reinterpret_cast<const uint32_t*>(perm), key.n, fr, st)
                         : (int)cudaMemcpyAsync(fr, dst, pbytes, cudaMemcpyDeviceToDevice, st);
+            if (rc) return rc;
+        }
+        if (fstats && key.n > 0) {
+            rc = launch_frame_stats(next, g.k, fstats + 3 * t, st);
+            if (rc) return rc;
+        }
+        if (nb && key.n > 0) {
+            double* msub = (double*)key.moved_sub;
+            rc = launch_gather_points(dst, 0, (const int64_t*)key.pick, sorted ? (const uint32_t*)perm : nullptr,
+                                      key.n_sub, msub, st);
+            if (!rc) rc = launch_trust((const double*)key.orig_sub, msub, key.n_sub, key.n_neighbors, nbstats + 2 * t, st);
+            if (!rc) rc = launch_order_pairs((const double*)key.orig_sub, msub, key.n_sub, nbstats + 2 * t + 1, st);
             if (rc) return rc;
         }
     }
@@ -451,19 +482,9 @@ int inim_run_stamped(float* pts, int64_t n, int k, int kernel_size, float backgr
     return rc ? rc : 1;
 }
 
-int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
-             float* frames, float* fields, float* disp, float* excursions, int* state, void* ws, cudaStream_t stream) {
-    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
-    if (kernel_size < 1) return INIM_EKERNEL;
-    if (stop_eps > 0.f && !state) return INIM_EINVAL;
-    if (iterations == 0) return 0;
-    RunKey key;
-    memset(&key, 0, sizeof(key));
-    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
-    key.iters = iterations; key.eps = stop_eps; key.frames = frames; key.fields = fields; key.disp = disp;
-    key.exc = excursions; key.state = state; key.ws = ws; key.st = stream;
-    if (n > 0 && use_mega(make_geo(k), kernel_size))  // a handful of launches: no graph needed
-        return enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
+// Replay the cached executable graph of `key`, capturing it on first use.
+static int run_graph(const RunKey& key, float* pts, float* frames, float* fields, float* disp, float* excursions,
+                     int* state, void* ws, cudaStream_t stream) {
     {
         std::lock_guard<std::mutex> lock(g_mu);
         for (auto& e : g_cache)
@@ -496,6 +517,71 @@ int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, in
         g_cache.push_back({key, exec});
     }
     return (int)cudaGraphLaunch(exec, stream);
+}
+
+int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
+             float* frames, float* fields, float* disp, float* excursions, int* state, void* ws, cudaStream_t stream) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    if (stop_eps > 0.f && !state) return INIM_EINVAL;
+    if (iterations == 0) return 0;
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations; key.eps = stop_eps; key.frames = frames; key.fields = fields; key.disp = disp;
+    key.exc = excursions; key.state = state; key.ws = ws; key.st = stream;
+    if (n > 0 && use_mega(make_geo(k), kernel_size))  // a handful of launches: no graph needed
+        return enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
+    return run_graph(key, pts, frames, fields, disp, excursions, state, ws, stream);
+}
+
+int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, float stop_eps,
+                     float* frames, float* fields, float* disp, float* excursions, int* state, void* ws,
+                     cudaStream_t stream, unsigned long long* frame_stats, const double* orig_sub, const int64_t* pick,
+                     int64_t n_sub, int n_neighbors, double* moved_sub, unsigned long long* nb_stats) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || iterations < 0 || !ws || (n > 0 && !pts) || !frame_stats) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    if (stop_eps > 0.f && !state) return INIM_EINVAL;
+    if (orig_sub && (!moved_sub || !nb_stats || n_sub < 2 || n_sub > n || n_neighbors < 1 || n_neighbors >= n_sub))
+        return INIM_EINVAL;
+    if (iterations == 0) return 0;
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations; key.eps = stop_eps; key.frames = frames; key.fields = fields; key.disp = disp;
+    key.exc = excursions; key.state = state; key.ws = ws; key.st = stream;
+    key.fstats = frame_stats;
+    if (orig_sub) {
+        key.orig_sub = orig_sub; key.pick = pick; key.n_sub = n_sub; key.n_neighbors = n_neighbors;
+        key.moved_sub = moved_sub; key.nbstats = nb_stats;
+    }
+    return run_graph(key, pts, frames, fields, disp, excursions, state, ws, stream);
+}
+
+int inim_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t stream) {
+    if (!k_ok(k) || !counts || !out3) return INIM_EINVAL;
+    return launch_frame_stats(counts, k, out3, stream);
+}
+
+int inim_gather_points(const void* pts, int pts_is_f64, const int64_t* rows, const uint32_t* perm, int64_t m,
+                       double* out, cudaStream_t stream) {
+    if (m < 0 || (m > 0 && (!pts || !out))) return INIM_EINVAL;
+    if (m == 0) return 0;
+    return launch_gather_points(pts, pts_is_f64, rows, perm, m, out, stream);
+}
+
+int inim_trust_penalty(const double* orig, const double* moved, int64_t n, int n_neighbors, unsigned long long* out,
+                       cudaStream_t stream) {
+    if (n < 0 || !out || n_neighbors < 1 || (n > 0 && (!orig || !moved)) || n_neighbors >= n) return INIM_EINVAL;
+    if ((size_t)n_neighbors * 16 > 200 * 1024) return INIM_EINVAL;
+    return launch_trust(orig, moved, n, n_neighbors, out, stream);
+}
+
+int inim_order_pairs(const double* orig, const double* moved, int64_t n, unsigned long long* out,
+                     cudaStream_t stream) {
+    if (n < 0 || !out || (n > 0 && (!orig || !moved))) return INIM_EINVAL;
+    if (n < 2) return 0;
+    return launch_order_pairs(orig, moved, n, out, stream);
 }
 
 int inim_run_uncached(float* pts, int64_t n, int k, int kernel_size, float background, int iterations,

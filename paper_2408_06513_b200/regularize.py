@@ -20,6 +20,7 @@ from . import _lib
 from .density import build_density, resolve_background
 from .errors import OutOfRangeLevel
 from .mapping import _defect_device, flat_response, sample_points
+from .metrics import RunMetrics, record_for_frame
 from .model import DeformationField, RegularizationParams, RegularizationRun, ScatterDataset
 
 CHUNK = 16  # iterations per captured graph
@@ -116,22 +117,25 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
         store_fields: bool = True, n_neighbors: int = 10) -> RegularizationRun:
     """Repeat iterations until the stopping criterion fires (regularize.py:40-80)."""
     params.validate()
-    if collect_metrics != "none":
-        raise NotImplementedError("collect_metrics='basic'/'full' needs the metrics subsystem, which is outside "
-                                  "this build's scope (SURVEY.md section 8(f)); use collect_metrics='none'")
     lib = D.require_cuda()
     result = RegularizationRun(dataset, params, store_fields=store_fields)
     flat_response.get(params.k)  # built once per run, as the reference (regularize.py:51)
     n = dataset.n
     k = params.k
     bg = resolve_background(params, n)
+    metrics = collect_metrics != "none"
+    full = collect_metrics == "full"
+    if metrics:  # frame 0 (regularize.py:53-57)
+        result.metrics.append(record_for_frame(0, dataset.positions, dataset.positions, k, wall_ms=0.0, full=full,
+                                               n_neighbors=n_neighbors))
     if params.iterations == 0:
         return result
     if params.stop == "time":
-        return _run_timed(result, dataset, params, bg)
+        return _run_timed(result, dataset, params, bg, collect_metrics, n_neighbors)
 
     chunk = min(CHUNK, params.iterations)
     b = _run_buffers(n, k, chunk, store_fields)
+    rm = RunMetrics(dataset.positions, k, chunk, full, n_neighbors) if metrics and n else None
     pts = b["pts"][:n] if n else b["pts"]
     if n:
         pts.copy_(D.to_device(dataset.positions).reshape(n, 2))
@@ -150,9 +154,14 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
         frames_needed = keep is None or any((done + t) in keep for t in range(1, c))
         frames = b["frames"] if frames_needed else None
         start_ev.record()
-        _lib.check(lib.inim_run(D.ptr(pts), n, k, params.kernel_size, bg, c, eps, D.ptr(frames),
-                                D.ptr(b["fields"]), D.ptr(b["disp"]), D.ptr(b["excs"]), D.ptr(state),
-                                D.ptr(b["ws"]), stream), "run")
+        if rm is None:
+            _lib.check(lib.inim_run(D.ptr(pts), n, k, params.kernel_size, bg, c, eps, D.ptr(frames),
+                                    D.ptr(b["fields"]), D.ptr(b["disp"]), D.ptr(b["excs"]), D.ptr(state),
+                                    D.ptr(b["ws"]), stream), "run")
+        else:
+            _lib.check(lib.inim_run_metrics(D.ptr(pts), n, k, params.kernel_size, bg, c, eps, D.ptr(frames),
+                                            D.ptr(b["fields"]), D.ptr(b["disp"]), D.ptr(b["excs"]), D.ptr(state),
+                                            D.ptr(b["ws"]), stream, *rm.args()), "run")
         end_ev.record()
         end_ev.synchronize()
         per_iter = start_ev.elapsed_time(end_ev) / 1e3 / c
@@ -174,13 +183,21 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
                 result._record(it, src_frame.clone())
             else:
                 result.iterations = it
+        if metrics:
+            if rm is not None:
+                result.metrics.extend(rm.records(done + 1, executed, per_iter * 1e3))
+            else:  # no samples: the reference's records of an empty layout
+                result.metrics.extend(record_for_frame(done + t + 1, dataset.positions, dataset.positions, k,
+                                                       wall_ms=per_iter * 1e3, full=full, n_neighbors=n_neighbors)
+                                      for t in range(executed))
         done += executed
         if stopped:
             break
     return result
 
 
-def _run_timed(result: RegularizationRun, dataset: ScatterDataset, params: RegularizationParams, bg: float):
+def _run_timed(result: RegularizationRun, dataset: ScatterDataset, params: RegularizationParams, bg: float,
+               collect_metrics: str = "none", n_neighbors: int = 10):
     """stop='time': the budget is host wall time, checked between iterations
     (regularize.py:62-63), so iterations are launched one at a time."""
     n = dataset.n
@@ -192,8 +209,13 @@ def _run_timed(result: RegularizationRun, dataset: ScatterDataset, params: Regul
         tick = time.perf_counter()
         new = _device_iterate(pos, params) if n else pos
         torch.cuda.synchronize()
-        result.wall_times.append(time.perf_counter() - tick)
+        wall = time.perf_counter() - tick
+        result.wall_times.append(wall)
         result._record(t, new)
+        if collect_metrics != "none":
+            result.metrics.append(record_for_frame(t, dataset.positions, new if n else dataset.positions, params.k,
+                                                   wall_ms=wall * 1e3, full=collect_metrics == "full",
+                                                   n_neighbors=n_neighbors))
         pos = new
     return result
 

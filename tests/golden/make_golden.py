@@ -1,7 +1,7 @@
 """Record golden vectors from the UNMODIFIED reference package (run in the build
 container, where /root/reference exists; the GPU box only reads the committed .npz).
 
-    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [metrics]
 
 The reference `uncrowd` package imports skimage at encodings.py:16, which is absent
 here, so a stub module is installed first; nothing on the
@@ -152,5 +152,52 @@ def main():
          n_iters=rd.iterations, last=rd.frame(rd.iterations))
 
 
+def metrics_cases():
+    """Layout metrics (metrics.py:46-168), including run(collect_metrics="full")."""
+    uc = import_reference()
+    from uncrowd import metrics as M
+
+    rng = np.random.default_rng(1789)
+    occ = {}
+    for k in (2, 4, 6, 8):
+        pts = np.concatenate([f32(rng.random((3000, 2))), three_cluster(2000, k),
+                              f32(np.array([[0, 0], [1, 1], [1, 0], [0, 1], [0.5, 0.5]] * 3))])
+        occ[f"pts_k{k}"] = pts
+        occ[f"binned_k{k}"] = M.binned_stddev(pts, k)
+        occ[f"over_k{k}"] = M.overplotting(pts, k)
+    grid = f32((np.stack(np.meshgrid(np.arange(16), np.arange(16)), -1).reshape(-1, 2) + 0.5) / 16)
+    occ.update(uniform=grid, binned_uniform=M.binned_stddev(grid, 4), over_uniform=M.overplotting(grid, 4))
+
+    # neighbourhood metrics: a perturbed layout with ties (duplicated points), n < cap
+    base = f32(rng.random((600, 2)))
+    base[100:110] = base[0]
+    moved = f32(np.clip(base + rng.normal(0, 0.02, base.shape), 0, 1))
+    nb = dict(orig=base, moved=moved,
+              trust10=M.trustworthiness(base, moved, 10), trust3=M.trustworthiness(base, moved, 3),
+              order=M.orthogonal_ordering(base, moved), trust_self=M.trustworthiness(base, base, 10),
+              order_self=M.orthogonal_ordering(base, base))
+    # subsampled ordering (n > cap)
+    big = f32(rng.random((6000, 2)))
+    bigm = f32(np.clip(big + rng.normal(0, 0.05, big.shape), 0, 1))
+    nb.update(big=big, bigm=bigm, order_big=M.orthogonal_ordering(big, bigm),
+              order_big_cap=M.orthogonal_ordering(big, bigm, sample_cap=1000))
+
+    # run with full metrics on the C1 layout (10k points > the 4096 subsample cap)
+    p10k = three_cluster(10_000, 2408)
+    run = uc.run(uc.ScatterDataset(positions=p10k), uc.RegularizationParams(k=8, kernel_size=8, iterations=3),
+                 collect_metrics="full")
+    recs = run.metrics
+    save("metrics", **{f"occ_{k}": v for k, v in occ.items()}, **{f"nb_{k}": v for k, v in nb.items()},
+         run_positions=p10k, run_k=8, run_iterations=3,
+         run_frames=np.stack([run.frame(t) for t in range(run.iterations + 1)]),
+         run_binned=np.array([r.binned_stddev for r in recs]), run_over=np.array([r.overplotting for r in recs]),
+         run_trust=np.array([r.trustworthiness for r in recs]), run_order=np.array([r.ordering for r in recs]),
+         run_json=np.array([r.to_json_line() for r in recs]))
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "metrics":
+        metrics_cases()
+    else:
+        main()
+        metrics_cases()

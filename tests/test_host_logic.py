@@ -148,6 +148,13 @@ def test_compute_without_gpu_raises_not_falls_back():
         P.accumulate(np.zeros((3, 2)), 4)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         P.build_integral_set(np.ones((8, 8)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.binned_stddev(np.full((3, 2), 0.5), 4)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.trustworthiness(np.random.rand(20, 2), np.random.rand(20, 2))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.run(P.ScatterDataset(positions=np.full((3, 2), 0.5)), P.RegularizationParams(k=4, iterations=1),
+              collect_metrics="full")
 
 
 def test_oracle_not_imported_by_product():
