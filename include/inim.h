@@ -217,6 +217,26 @@ int inim_trust_penalty(const double* orig, const double* moved, int64_t n, int n
 int inim_order_pairs(const double* orig, const double* moved, int64_t n, unsigned long long* out,
                      cudaStream_t stream);
 
+/* transition_positions (regularize.py:83-93) as the service's float32 payload
+ * (service.py:170-172): out[q] = f32((1 - frac) * lo[q] + frac * hi[q]) computed in
+ * float64 (out = f32(lo) when `same`, i.e. an integer level).  lo / hi are float64
+ * (flag 1) or float32 device arrays of `count` values. */
+int inim_blend_frames(const void* lo, int lo_f64, const void* hi, int hi_f64, int64_t count, double frac, int same,
+                      float* out, cudaStream_t stream);
+
+/* Scratch bytes of inim_deform_background for a 2^k grid (0 if k outside 1..13). */
+size_t inim_deform_background_scratch_bytes(int k);
+
+/* deform_background (encodings.py:124-162): targets = the 4^k source pixel coordinates
+ * (x = i/s, y = j/s, row-major) pushed through the composed fields (float32 (m, 2)),
+ * values = the iteration-0 density (float32 (s, s)).  out (float64 (s, s)) = the
+ * weight-normalised bilinear splat of the values at the targets, summed per pixel in
+ * the reference's np.add.at order (bit-identical sums for identical inputs); pixels
+ * without weight copy their nearest covered pixel (exact Euclidean distance transform).
+ * range2 (device float[2]) receives min and max of the (positive) values. */
+int inim_deform_background(const float* targets, const float* values, int k, double* out, float* range2,
+                           void* scratch, cudaStream_t stream);
+
 /* Host-buffer end-to-end call (the FFI a C/ctypes caller of the reference would bind):
  * pts_host (n,2) float64 in, final positions float64 out (may alias), `iterations`
  * fixed iterations.  Allocates and frees its own device memory; synchronises. */

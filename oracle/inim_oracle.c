@@ -590,3 +590,51 @@ int orc_order_pairs(const double* orig, const double* moved, int64_t n, int64_t*
     *out = kept;
     return 0;
 }
+
+/* ============================================================ deform_background
+ * encodings.py:141-156: cell / fractions of every mapped source pixel, then the four
+ * np.add.at passes in order, each sequential over the sources (unbuffered in-place
+ * accumulation), then acc / weight on covered pixels.  covered[p] = weight > 0.  The
+ * nearest-covered fill (scipy distance_transform_edt) is done by the Python wrapper
+ * with the reference's own scipy call.
+ */
+int orc_background_splat(const double* targets, const double* values, int k, double* out, unsigned char* covered) {
+    if (k < 1 || k > 14) return 1;
+    const int64_t s = (int64_t)1 << k, m = s * s;
+    double* acc = (double*)calloc((size_t)m, sizeof(double));
+    double* wgt = (double*)calloc((size_t)m, sizeof(double));
+    int64_t* cell = (int64_t*)malloc(sizeof(int64_t) * 2 * (size_t)m);
+    double* frac = (double*)malloc(sizeof(double) * 2 * (size_t)m);
+    if (!acc || !wgt || !cell || !frac) {
+        free(acc); free(wgt); free(cell); free(frac);
+        return 2;
+    }
+    for (int64_t q = 0; q < m; ++q)
+        for (int a = 0; a < 2; ++a) {
+            const double sc = targets[2 * q + a] * (double)s;
+            double c = floor(sc);
+            if (c < 0.0) c = 0.0;
+            if (c > (double)(s - 2)) c = (double)(s - 2);
+            double f = sc - c;
+            if (f < 0.0) f = 0.0;
+            if (f > 1.0) f = 1.0;
+            cell[2 * q + a] = (int64_t)c;
+            frac[2 * q + a] = f;
+        }
+    for (int pass = 0; pass < 4; ++pass) {
+        const int di = pass & 1, dj = pass >> 1;
+        for (int64_t q = 0; q < m; ++q) {
+            const double fx = frac[2 * q], fy = frac[2 * q + 1];
+            const double w = (di ? fx : 1.0 - fx) * (dj ? fy : 1.0 - fy);
+            const int64_t p = (cell[2 * q + 1] + dj) * s + cell[2 * q] + di;
+            acc[p] += w * values[q];
+            wgt[p] += w;
+        }
+    }
+    for (int64_t p = 0; p < m; ++p) {
+        covered[p] = wgt[p] > 0.0;
+        out[p] = covered[p] ? acc[p] / wgt[p] : 0.0;
+    }
+    free(acc); free(wgt); free(cell); free(frac);
+    return 0;
+}

@@ -336,3 +336,41 @@ def record_for_frame(original, positions, k: int, full: bool = False, n_neighbor
         order = orthogonal_ordering(o, m)
     pos = _f64(positions).reshape(-1, 2)
     return (binned_stddev(pos, k), overplotting(pos, k) if len(pos) else 0.0, trust, order)
+
+
+# --------------------------------------------------------------- deform_background
+def background_splat(targets, values, k: int):
+    """encodings.py:141-156 -> (out, covered): the weight-normalised bilinear splat
+    before the nearest-covered fill."""
+    t = _f64(targets).reshape(-1, 2)
+    v = _f64(values).ravel()
+    s = 1 << k
+    out = np.empty((s, s))
+    cov = np.empty((s, s), dtype=np.uint8)
+    L = lib()
+    L.orc_background_splat.argtypes = [_dp, _dp, ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_ubyte)]
+    _check(L.orc_background_splat(_p(t), _p(v), k, _p(out), cov.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte))),
+           "background_splat")
+    return out, cov.astype(bool)
+
+
+def background_fill(out, covered):
+    """encodings.py:157-159: uncovered pixels copy their nearest covered pixel, through
+    the reference's own dependency (scipy.ndimage.distance_transform_edt)."""
+    from scipy.ndimage import distance_transform_edt
+
+    out = out.copy()
+    if not covered.all():
+        dist, (jn, in_) = distance_transform_edt(~covered, return_indices=True)
+        out[~covered] = out[jn[~covered], in_[~covered]]
+    else:
+        dist = np.zeros(covered.shape)
+    return out, dist
+
+
+def deform_background(targets, values, k: int):
+    """encodings.deform_background (encodings.py:124-162) from the mapped source pixel
+    coordinates and the iteration-0 density values -> (values, distance of every pixel
+    to its nearest covered pixel)."""
+    out, cov = background_splat(targets, values, k)
+    return background_fill(out, cov)

@@ -67,6 +67,9 @@ _SIGS = {
     "inim_gather_points": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
     "inim_trust_penalty": (c_int, [c_void_p, c_void_p, c_i64, c_int, c_void_p, c_void_p]),
     "inim_order_pairs": (c_int, [c_void_p, c_void_p, c_i64, c_void_p, c_void_p]),
+    "inim_deform_background_scratch_bytes": (c_size_t, [c_int]),
+    "inim_deform_background": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "inim_blend_frames": (c_int, [c_void_p, c_int, c_void_p, c_int, c_i64, c_double, c_int, c_void_p, c_void_p]),
 }
 
 INIM_EINVAL, INIM_ENOTPOW2, INIM_EKERNEL, INIM_EDRIVER = -1, -2, -3, -4

@@ -181,6 +181,19 @@ __global__ void flat_response_f64_kernel(int k, double* __restrict__ defect) {
     defect[2 * q + 1] = __dmul_rn(ty, inv);
 }
 
+// transition_positions (regularize.py:83-93) rounded to float32 for the service's
+// binary payload (service.py:170-172): (1 - frac) * lo + frac * hi in float64, each
+// operation rounded as numpy does (no FMA), then one rounding to float32.
+template <typename TL, typename TH>
+__global__ void blend_frames_kernel(const TL* __restrict__ lo, const TH* __restrict__ hi, int64_t count, double frac,
+                                    int same, float* __restrict__ out) {
+    const double wl = 1.0 - frac;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < count; q += (int64_t)gridDim.x * blockDim.x) {
+        const double a = (double)lo[q];
+        out[q] = __double2float_rn(same ? a : __dadd_rn(__dmul_rn(wl, a), __dmul_rn(frac, (double)hi[q])));
+    }
+}
+
 }  // namespace inim
 
 using namespace inim;
@@ -223,6 +236,22 @@ int inim_flat_response_f64(int k, double* defect, cudaStream_t stream) {
     if (k < 0 || k > INIM_MAX_K || !defect) return INIM_EINVAL;
     const int64_t m = (int64_t)1 << (2 * k);
     flat_response_f64_kernel<<<(unsigned)((m + 255) / 256), 256, 0, stream>>>(k, defect);
+    return (int)cudaGetLastError();
+}
+
+int inim_blend_frames(const void* lo, int lo_f64, const void* hi, int hi_f64, int64_t count, double frac, int same,
+                      float* out, cudaStream_t stream) {
+    if (count < 0 || (count > 0 && (!lo || !hi || !out))) return INIM_EINVAL;
+    if (count == 0) return 0;
+    const unsigned g = (unsigned)((count + 255) / 256 < 4096 ? (count + 255) / 256 : 4096);
+    if (lo_f64 && hi_f64)
+        blend_frames_kernel<<<g, 256, 0, stream>>>((const double*)lo, (const double*)hi, count, frac, same, out);
+    else if (lo_f64)
+        blend_frames_kernel<<<g, 256, 0, stream>>>((const double*)lo, (const float*)hi, count, frac, same, out);
+    else if (hi_f64)
+        blend_frames_kernel<<<g, 256, 0, stream>>>((const float*)lo, (const double*)hi, count, frac, same, out);
+    else
+        blend_frames_kernel<<<g, 256, 0, stream>>>((const float*)lo, (const float*)hi, count, frac, same, out);
     return (int)cudaGetLastError();
 }
 

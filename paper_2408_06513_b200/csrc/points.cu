@@ -416,6 +416,15 @@ int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* count
     return (int)cudaGetLastError();
 }
 
+// Exclusive prefix of m (a multiple of 4) u32 counts into `out`; bsum: sort_bsum_words.
+int launch_exclusive_scan_u32(const uint32_t* counts, int64_t m, uint32_t* bsum, uint32_t* out, cudaStream_t st) {
+    const unsigned nb = (unsigned)((m + kScanBlock - 1) / kScanBlock);
+    INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb), dim3(256), 0, st, counts, m, bsum));
+    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb));
+    INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb), dim3(256), 0, st, counts, m, (const uint32_t*)bsum, out));
+    return (int)cudaGetLastError();
+}
+
 size_t sort_bsum_words(int k) { return (size_t)((((int64_t)1 << (2 * k)) + kScanBlock - 1) / kScanBlock); }
 
 int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st) {

@@ -253,16 +253,24 @@ def map_through(fields, points: np.ndarray, upto: Optional[int] = None) -> np.nd
         for f in chosen:
             out = sample_points(f, out, clip=True)
         return out
-    lib = D.require_cuda()
     shape = out.shape
     flat = out.reshape(-1, 2)
-    n = len(flat)
-    if n == 0:
+    if len(flat) == 0:
         return out
-    a = D.to_device(flat)
+    return D.to_host64(map_through_device(chosen, D.to_device(flat))).reshape(shape)
+
+
+def map_through_device(fields, pts: torch.Tensor) -> torch.Tensor:
+    """Float32 device points (n, 2) pushed through float32 device fields (sample +
+    clip per field, the run's own move arithmetic); returns a new device tensor."""
+    lib = D.require_cuda()
+    n = pts.shape[0]
+    a = pts.contiguous().clone()
+    if n == 0 or not fields:
+        return a
     bbuf = torch.empty_like(a)
-    for f in chosen:
+    for f in fields:
         _lib.check(lib.inim_sample(D.ptr(f.device_targets()), f.k, D.ptr(a), D.ptr(bbuf), n, 1, None, D.stream()),
                    "map_through")
         a, bbuf = bbuf, a
-    return D.to_host64(a).reshape(shape)
+    return a

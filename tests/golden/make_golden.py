@@ -1,7 +1,7 @@
 """Record golden vectors from the UNMODIFIED reference package (run in the build
 container, where /root/reference exists; the GPU box only reads the committed .npz).
 
-    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [metrics]
+    NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_golden.py [metrics|encodings]
 
 The reference `uncrowd` package imports skimage at encodings.py:16, which is absent
 here, so a stub module is installed first; nothing on the
@@ -195,9 +195,52 @@ def metrics_cases():
          run_json=np.array([r.to_json_line() for r in recs]))
 
 
+def encodings_cases():
+    """deform_grid / deform_background / field dumps (encodings.py:55-162,
+    fileio.py:63-104, service.py:170-172) on the reference test suite's blob run
+    (test_encodings.py:32-37), with the intermediates the oracle is pinned on."""
+    uc = import_reference()
+    import io
+    import tempfile
+
+    from uncrowd import encodings as E, fileio
+    from uncrowd.density import build_density
+
+    gen = np.random.default_rng(11)
+    pts = f32(np.clip(gen.normal((0.35, 0.5), 0.04, (2000, 2)), 0.0, 1.0))
+    ds = uc.validate_dataset(pts, normalize=False)
+    run = uc.run(ds, uc.RegularizationParams(k=7, kernel_size=8, iterations=4))
+    k = 7
+    X, Y = uc.model.unit_coordinates(k)
+    sources = np.column_stack([X.ravel(), Y.ravel()])
+    targets = uc.map_through(run.fields, sources)
+    dens = build_density(run.frame(0), run.params)
+    bg = E.deform_background(run)
+    bg2 = E.deform_background(run, upto=2)
+    grid = E.deform_grid(run, spacing=16, subdivision=4)
+    with tempfile.TemporaryDirectory() as tmp:
+        fileio.export_field(run.fields[-1], f"{tmp}/f.bin", iteration=4)
+        field_bytes = open(f"{tmp}/f.bin", "rb").read()
+        fileio.export_grid(dens.values, f"{tmp}/g.bin", k=k, index=3)
+        grid_bytes = open(f"{tmp}/g.bin", "rb").read()
+    payload = {f"payload_{str(lv).replace('.', '_')}": np.frombuffer(
+        uc.transition_positions(run, lv).astype("<f4").tobytes(), dtype=np.uint8) for lv in (0, 1.25, 2.5, 4)}
+    save("encodings", positions=pts, k=k, iterations=4,
+         frames=np.stack([run.frame(t) for t in range(run.iterations + 1)]),
+         fields=np.stack([f.targets for f in run.fields]),
+         targets=targets, density=dens.values, background=bg.values, background_range=np.array(bg.value_range),
+         background_upto2=bg2.values,
+         grid_sizes=np.array([len(line) for line in grid.polylines]), grid=np.concatenate(grid.polylines),
+         field_bytes=np.frombuffer(field_bytes, dtype=np.uint8), grid_bytes=np.frombuffer(grid_bytes, dtype=np.uint8),
+         **payload)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "metrics":
         metrics_cases()
+    elif len(sys.argv) > 1 and sys.argv[1] == "encodings":
+        encodings_cases()
     else:
         main()
         metrics_cases()
+        encodings_cases()
