@@ -51,13 +51,11 @@ INIM_DEV float warp_max(float v) {
 }
 
 // Half-sample symmetric reflection with period 2n (scipy.ndimage mode="reflect";
-// reference density.py:49-50, restated in tests/oracles.py:95-102).
+// reference density.py:49-50, restated in tests/oracles.py:95-102).  n is a power of
+// two (every grid side is 2^k), so the residue mod 2n is a mask, negative idx included.
 INIM_DEV int reflect_index(int idx, int n) {
-    int p = 2 * n;
-    idx %= p;
-    if (idx < 0) idx += p;
-    if (idx >= n) idx = p - 1 - idx;
-    return idx;
+    idx &= 2 * n - 1;
+    return idx >= n ? 2 * n - 1 - idx : idx;
 }
 
 // Non-negative float max through integer atomics (bit patterns of non-negative IEEE

@@ -113,7 +113,9 @@ struct Chain {
     __device__ __forceinline__ int col(int b) const {
         return KIND == 0 ? kk : (KIND == 1 ? kk - (g.B - b) * g.TH : kk - b * g.TH);
     }
-    // step b -> b + 1, b in [lo, hi): the column col(b + 1) is inside the grid
+    // step b -> b + 1, b in [lo, hi): the column col(b + 1) is inside the grid.  BP = false
+    // leaves out the X2 border injection (added later by border_term once bp is ready).
+    template <bool BP = true>
     __device__ __forceinline__ double term(int b) const {
         const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX, tl = g.twlog;
         const double* __restrict__ tilepre = ws.tilepre;
@@ -135,8 +137,11 @@ struct Chain {
         if (c > 0) v += (double)__ldg(inpre + q - 1) + tilepre[b * NX + ((c - 1) >> tl)];
         const int rq = TH - 1 - (TW - u);
         if (rq >= 0 && x < NX - 1) v += (double)__ldg(ws.ure + ((b * NX + x + 1) * TH + rq));
-        if (c + TH >= s) v += bp[b];  // the chain enters the grid: X2_b beyond the border
+        if (BP && c + TH >= s) v += bp[b];  // the chain enters the grid: X2_b beyond the border
         return v;
+    }
+    __device__ __forceinline__ double border_term(int b) const {  // KIND 2: the BP part of term(b)
+        return col(b + 1) + g.TH >= g.s ? bp[b] : 0.0;
     }
     __device__ __forceinline__ void emit(int b, double run) const {
         const int s = g.s, TH = g.TH;
@@ -195,6 +200,61 @@ __device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, 
         T.emit(b, run);
         if (b < T.hi) run += T.term(b);
     }
+}
+
+// Single-read variant (the standalone chains kernel): the band range of each chain's
+// step terms is split into NY chunks of at most MAXCH terms; each thread loads its
+// chunk's terms once into registers (all loads in flight together, issued before the
+// X2 items' band prefix so its latency overlaps them), then scans them.  X2 items
+// compute the band prefix into bp here; `publish` stores it and the total.
+template <int KIND, int MAXCH>
+__device__ __forceinline__ void chains_body_reg(const Geo& g, const Ws& ws, int kk, double (*part)[33], double* bp,
+                                                double* sh, bool publish) {
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, NY = blockDim.x >> 5;
+    const bool live = kk < (KIND == 0 ? g.s : g.s + g.B * g.TH);
+    const Chain<KIND> T(g, ws, bp, kk);
+    const int nt = live && T.hi > T.lo ? T.hi - T.lo : 0;  // step terms b in [lo, hi)
+    const int CH = (g.B + NY - 1) / NY;                    // <= MAXCH (host dispatch)
+    const int b0 = T.lo + min(nt, ty * CH), b1 = T.lo + min(nt, ty * CH + CH);
+    double t[MAXCH];
+#pragma unroll
+    for (int q = 0; q < MAXCH; ++q) t[q] = b0 + q < b1 ? T.template term<false>(b0 + q) : 0.0;
+    if (KIND == 2) {
+        band_prefix(g, ws, bp, sh);
+        if (publish) {
+            for (int q = threadIdx.x; q <= g.B; q += blockDim.x) ws.bandpre[q] = bp[q];
+            if (threadIdx.x == 0) *ws.total = bp[g.B];
+        }
+#pragma unroll
+        for (int q = 0; q < MAXCH; ++q)
+            if (b0 + q < b1) t[q] += T.border_term(b0 + q);
+    }
+    double loc = 0.0;
+#pragma unroll
+    for (int q = 0; q < MAXCH; ++q) loc += t[q];
+    part[ty][tx] = loc;
+    __syncthreads();
+    double run = 0.0;
+    for (int q = 0; q < ty; ++q) run += part[q][tx];
+#pragma unroll
+    for (int q = 0; q < MAXCH; ++q) {
+        if (b0 + q < b1) {
+            T.emit(b0 + q, run);
+            run += t[q];
+        }
+    }
+    // the value after the last step (band hi) belongs to the chunk holding the last term
+    if (live && T.hi >= T.lo && ((nt > 0 && b0 < b1 && b1 == T.hi) || (nt == 0 && ty == 0))) T.emit(T.hi, run);
+}
+
+template <int MAXCH>
+__device__ __forceinline__ void chains_item_reg(const Geo& g, const Ws& ws, int item, double (*part)[33], double* bp,
+                                                double* sh) {
+    const int tx = threadIdx.x & 31;
+    const int ntl = chain_groups_tl(g), nxg = chain_groups_x(g);
+    if (item < ntl) chains_body_reg<0, MAXCH>(g, ws, item * 32 + tx, part, bp, sh, false);
+    else if (item < ntl + nxg) chains_body_reg<1, MAXCH>(g, ws, (item - ntl) * 32 + tx, part, bp, sh, false);
+    else chains_body_reg<2, MAXCH>(g, ws, (item - ntl - nxg) * 32 + tx, part, bp, sh, item == ntl + nxg);
 }
 
 // bp: the band prefix (band_prefix) for X2 items, else unused.

@@ -110,17 +110,15 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
                 for (int e = 0; e < NP4; ++e) {
                     const int c = 4 * (lane + 32 * e);
                     if (r < RH && c < W) {
+                        // the four components go out in a lane-rotated order: with ld = RH + 1
+                        // lanes c4 and c4 + 8 share a bank for the same component, so lane
+                        // group (lane >> 3) starts at component (lane >> 3) (conflict-free)
                         const uint4 u = v4[q][e];
-                        if (sizeof(T) == 4 && std::is_same<T, float>::value) {
-                            sh[c * ld + r] = __uint_as_float(u.x);
-                            sh[(c + 1) * ld + r] = __uint_as_float(u.y);
-                            sh[(c + 2) * ld + r] = __uint_as_float(u.z);
-                            sh[(c + 3) * ld + r] = __uint_as_float(u.w);
-                        } else {
-                            sh[c * ld + r] = (float)u.x;
-                            sh[(c + 1) * ld + r] = (float)u.y;
-                            sh[(c + 2) * ld + r] = (float)u.z;
-                            sh[(c + 3) * ld + r] = (float)u.w;
+#pragma unroll
+                        for (int kq = 0; kq < 4; ++kq) {
+                            const int comp = (kq + (lane >> 3)) & 3;
+                            const uint32_t bits = comp == 0 ? u.x : (comp == 1 ? u.y : (comp == 2 ? u.z : u.w));
+                            sh[(c + comp) * ld + r] = std::is_same<T, float>::value ? __uint_as_float(bits) : (float)bits;
                         }
                     }
                 }
@@ -170,9 +168,9 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
     }
     __syncthreads();
     if ((TWH & 3) == 0) {  // 16-byte stores of the output tile
-        const int TW4 = TWH >> 2;
+        const int TW4 = TWH >> 2, l4 = 31 - __clz(TW4);  // TWH is a power of two
         for (int q = threadIdx.x; q < RH * TW4; q += blockDim.x) {
-            const int r = q / TW4, c = 4 * (q - r * TW4);
+            const int r = q >> l4, c = 4 * (q & (TW4 - 1));
             const float* sr = so + r * (TWH + 1) + c;
             *reinterpret_cast<float4*>(out + (int64_t)(j0 + r) * s + i0 + c) = make_float4(sr[0], sr[1], sr[2], sr[3]);
         }
@@ -265,9 +263,9 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     }
     // the VR x TW tile of d out
     if ((TW & 3) == 0) {
-        const int TW4 = TW >> 2;
+        const int TW4 = TW >> 2, l4 = 31 - __clz(TW4);  // TW is a power of two
         for (int q = threadIdx.x; q < VR * TW4; q += blockDim.x) {
-            const int r = q / TW4, c4 = q - r * TW4;
+            const int r = q >> l4, c4 = q & (TW4 - 1);
             reinterpret_cast<float4*>(d + (int64_t)(a0 + r) * s + i0)[c4] = reinterpret_cast<const float4*>(sd)[q];
         }
     } else {
