@@ -151,7 +151,8 @@ def algorithmic_bytes(name: str, n: int, m: int) -> int:
 
 # ncu kernel names -> the names inim_profile_run reports
 NCU_NAMES = {"sample_f32_kernel": "sample", "write_kernel": "write_field", "smooth_h_kernel": "smooth_h",
-             "smooth_v_kernel": "smooth_v_reduce", "chains_kernel": "chains", "splat_f32_kernel": "splat"}
+             "smooth_v_kernel": "smooth_v_reduce", "chains_kernel": "chains", "splat_f32_kernel": "splat",
+             "lines_kernel": "lines"}
 
 
 def ncu_traffic(workload: str):
@@ -299,7 +300,8 @@ def bench_ours(args):
                    "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": f"splom-shard x{world}" if world > 1 else "single plot"},
         "e2e": e2e,
-        "gpu_launches": int(args.steps * (ITERS * lib.inim_kernels_per_iteration(k) + 1)),
+        "gpu_launches": int(args.steps * sum(v["launches_per_step"] for nm, v in kernels.items()
+                                             if nm != "memset_counts")),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
                      "traffic": ncu_traffic("c3" if c3 else "c2").get(dom),

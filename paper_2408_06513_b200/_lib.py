@@ -98,7 +98,8 @@ def load(path: Path | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # INIM_LIB_PATH: an alternative build of the same ABI (A/B timing experiments)
+    p = Path(path) if path else Path(os.environ.get("INIM_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise RuntimeError(f"libinim.so not built ({p}); run paper_2408_06513_b200._lib.build() "
                            "or `make -C paper_2408_06513_b200/csrc` -- there is no CPU fallback")

@@ -357,7 +357,6 @@ int inim_integral_set(const float* d, int k, float* tables8, double* total, void
         if (rc) return rc;
         mp = &map;
     }
-    INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, stream));  // reduce's band counters
     int rc = launch_reduce_from_global(d, g, w, mp, stream);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, w, nullptr, stream);
@@ -393,7 +392,6 @@ int inim_field_from_density(const float* d, int k, const float* defect, float* t
         if (rc) return rc;
         mp = &map;
     }
-    INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, stream));  // reduce's band counters
     int rc = launch_reduce_from_global(d, g, w, mp, stream);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, w, nullptr, stream);
@@ -688,12 +686,11 @@ int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, in
 }
 
 int inim_kernels_per_iteration(int k) {
-    // smooth_h, smooth_v(+reduce), 3 carry-scan kernels (lines, chains, marg),
-    // write_field, move (+ iter_end when the displacement criterion is on).  The move
-    // of iteration t splats iteration t+1, so a run adds one splat kernel and one memset
-    // node in total.
+    // smooth_h, smooth_v(+reduce), lines, chains, write_field, move (+ iter_end when the
+    // displacement criterion is on).  The move of iteration t splats iteration t+1, so a
+    // run adds one splat kernel (plus the point sort and unpermute) and a memset node.
     (void)k;
-    return 7;
+    return 6;
 }
 
 }  // extern "C"

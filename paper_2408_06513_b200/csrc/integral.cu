@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_ring_kernel(const __
                 issue(kq + 2);
             }
         }
-        red.template finish<true>();
+        red.template finish<false>();  // band lines: lines_kernel
     }
 }
 
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* 
     const int tile = blockIdx.x * kWarpsPerCta + w;
     if (tile >= g.B * g.NX) return;
     const int b = tile / g.NX, x = tile - b * g.NX;
-    warp_tile_reduce<CPL, true, true>(d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW, g.s, g, ws, b, x, lane);
+    warp_tile_reduce<CPL, false, true>(d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW, g.s, g, ws, b, x, lane);
 }
 
 // The write pass re-reads its tile straight from global memory (rows prefetched two

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kMegaThreads, 2)
         stamp(t);
         // ---- smoothing, vertical + background + tile reduce
         for (int item = blockIdx.x; item < nV; item += gridDim.x)
-            smooth_v_tile<R>(A.ws.tmp, A.d, g, A.v, A.ws, A.taps, A.bg, 1, item % g.NX, item / g.NX,
+            smooth_v_tile<R>(A.ws.tmp, A.d, g, A.v, A.ws, A.taps, A.bg, 2, item % g.NX, item / g.NX,
                              reinterpret_cast<float*>(smem));
         fence_proxy_async_global();  // d (generic-proxy stores) is read by TMA in the field phase
         grid.sync();

@@ -3,6 +3,7 @@
 // completes a band) and the marginals are read off the chains by the write pass, so
 // phase 2 is one launch over 1/TH of the texture.
 #include "inim_scan.cuh"
+#include "inim_tiles.cuh"
 
 namespace inim {
 
@@ -34,7 +35,35 @@ __global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws w
     chains_item_reg<MAXCH>(g, ws, blockIdx.x, part, bp, sh);
 }
 
+// Band lines (one CTA per band, one warp per row): HC[j][x] = exclusive prefix over the
+// tiles of row j's tile row sums, rpre = the band's in-band prefix of the row totals,
+// tilepre / btot = the exclusive prefix and the total of the band's tile totals.  A
+// launch of its own so that no reduce warp has to fence and count its band's arrivals.
+__global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws, const int* state) {
+    pdl_enter();
+    if (state && state[0]) return;
+    __shared__ double rowtot[32];
+    const int b = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TH = g.TH, NX = g.NX, a = b * TH;
+    {
+        const double t = warp_line_prefix(ws.rowsum + (int64_t)(a + w) * NX, ws.hc + (int64_t)(a + w) * NX, NX, lane);
+        if (lane == 0) rowtot[w] = t;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const double v = lane < TH ? rowtot[lane] : 0.0;
+        const double inc = warp_inclusive_scan_d(v, lane);
+        if (lane < TH) ws.rpre[a + lane] = inc;
+    }
+    if (w == (TH > 1 ? 1 : 0)) {
+        const double bt = warp_line_prefix(ws.tiletot + (int64_t)b * NX, ws.tilepre + (int64_t)b * NX, NX, lane);
+        if (lane == 0) ws.btot[b] = bt;
+    }
+}
+
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st) {
+    INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B), dim3(32 * g.TH), 0, st, g, ws, state));
+    prof_mark(st, "lines");
     const int ny = chain_warps(g), ch = (g.B + ny - 1) / ny;
     const dim3 grid(chains_items(g)), block(32 * ny);
     // register-held chunks pay off only while they are short (measured: 1024^2 +7% on

@@ -84,7 +84,7 @@ template <int KS>
 static int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
     constexpr int R = 3 * KS;
-    uint32_t* ctr = emit ? ws.bandctr : nullptr;
+    uint32_t* ctr = nullptr;  // the standalone reduce has no band counters (lines_kernel)
     int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next,
                                             ctr, g.B, st)
                     : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, ctr,
