@@ -117,26 +117,34 @@ struct Chain {
     // leaves out the X2 border injection (added later by border_term once bp is ready).
     template <bool BP = true>
     __device__ __forceinline__ double term(int b) const {
+        // The in-tile aggregates (inpre, ulbot, urbot, ule, ure: sums over at most one
+        // TH x TW tile) are combined in float32 and converted once; only the tile prefix
+        // tilepre (a band-wide sum) is added in float64.  Indices stay below B * s <= 2^24.
         const int s = g.s, TH = g.TH, TW = g.TW, NX = g.NX, tl = g.twlog;
         const double* __restrict__ tilepre = ws.tilepre;
         const float* __restrict__ inpre = ws.inpre;
         if (KIND == 0) {
-            const int64_t q = (int64_t)b * s + kk;
+            const int q = b * s + kk;
             return tilepre[b * NX + (kk >> tl)] + (double)__ldg(inpre + q);
         }
         const int c = col(b + 1);
         const int x = c >> tl, u = c & (TW - 1);
-        const int64_t q = (int64_t)b * s + c;
+        const int q = b * s + c;
         if (KIND == 1) {
-            double v = (double)__ldg(ws.ulbot + q) - ((double)__ldg(inpre + q) + tilepre[b * NX + x]);
+            float f = __ldg(ws.ulbot + q) - __ldg(inpre + q);
             const int rr = TH - 2 - u;  // row where the chain leaves the tile on the left
-            if (rr >= 0 && x > 0) v += (double)__ldg(ws.ule + ((b * NX + x - 1) * TH + rr));
-            return v;
+            if (rr >= 0 && x > 0) f += __ldg(ws.ule + ((b * NX + x - 1) * TH + rr));
+            return (double)f - tilepre[b * NX + x];
         }
-        double v = (double)__ldg(ws.urbot + q);
-        if (c > 0) v += (double)__ldg(inpre + q - 1) + tilepre[b * NX + ((c - 1) >> tl)];
+        float f = __ldg(ws.urbot + q);
+        double t = 0.0;
+        if (c > 0) {
+            f += __ldg(inpre + q - 1);
+            t = tilepre[b * NX + ((c - 1) >> tl)];
+        }
         const int rq = TH - 1 - (TW - u);
-        if (rq >= 0 && x < NX - 1) v += (double)__ldg(ws.ure + ((b * NX + x + 1) * TH + rq));
+        if (rq >= 0 && x < NX - 1) f += __ldg(ws.ure + ((b * NX + x + 1) * TH + rq));
+        double v = (double)f + t;
         if (BP && c + TH >= s) v += bp[b];  // the chain enters the grid: X2_b beyond the border
         return v;
     }
