@@ -54,15 +54,19 @@ def workspace(k: int, n: int = 0) -> torch.Tensor:
     return ws
 
 
-def to_device(a, dtype=torch.float32) -> torch.Tensor:
-    """Host array (any float dtype) -> contiguous device tensor of `dtype`."""
+def to_device(a, dtype=torch.float32, out: torch.Tensor = None) -> torch.Tensor:
+    """Host array (any float dtype) -> contiguous device tensor of `dtype` (float32:
+    optionally cast straight into `out`, a contiguous float32 tensor of a.size)."""
     if isinstance(a, torch.Tensor):
         return a.to(device=device(), dtype=dtype).contiguous()
     arr = np.ascontiguousarray(a)
     if dtype == torch.float32:
         # ship float64 as-is and narrow on the device (one cast kernel)
         src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device(), non_blocking=False)
-        out = torch.empty(src.shape, dtype=torch.float32, device=device())
+        if out is None:
+            out = torch.empty(src.shape, dtype=torch.float32, device=device())
+        elif not (out.dtype == torch.float32 and out.is_contiguous() and out.numel() == src.numel()):
+            raise ValueError("to_device: `out` must be a contiguous float32 tensor of the same size")
         lib = require_cuda()
         _lib.check(lib.inim_cast_f64_to_f32(ptr(src), ptr(out), src.numel(), stream()), "cast")
         return out
@@ -84,3 +88,17 @@ def to_host64(t: torch.Tensor) -> np.ndarray:
     host = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
     host.copy_(out)
     return host.numpy()
+
+
+def to_host64_async(t: torch.Tensor):
+    """Start the device->host float64 copy of a float32 device tensor; returns
+    (pinned host tensor, CUDA event).  The host data is valid once the event completes."""
+    lib = require_cuda()
+    t = t.contiguous()
+    out = torch.empty(t.shape, dtype=torch.float64, device=t.device)
+    _lib.check(lib.inim_cast_f32_to_f64(ptr(t), ptr(out), t.numel(), stream()), "cast")
+    host = torch.empty(t.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(out, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return host, ev

@@ -243,6 +243,7 @@ class RegularizationRun:
         self.metrics: list = []
         self._dev_frames: dict = {}      # t -> float32 (n, 2) device tensor (t >= 1)
         self._host_frames: dict = {0: dataset.positions}
+        self._pending: dict = {}         # t -> (pinned host tensor, event): copy in flight
         self._stride = 1
         self.iterations = 0
         self.wall_times: list = []
@@ -258,6 +259,15 @@ class RegularizationRun:
                 if i not in keep:
                     del self._dev_frames[i]
                     self._host_frames.pop(i, None)
+                    self._pending.pop(i, None)
+
+    def _prefetch(self, t: int):
+        """Start the host copy of kept frame t now (the run's last frame): it overlaps
+        the host-side bookkeeping, and frame(t) only waits for it."""
+        from ._device import to_host64_async
+
+        if t in self._dev_frames and t not in self._host_frames and t not in self._pending:
+            self._pending[t] = to_host64_async(self._dev_frames[t])
 
     def _device_frame(self, t: int):
         from ._device import to_device
@@ -271,6 +281,11 @@ class RegularizationRun:
         if not 0 <= t <= self.iterations:
             raise OutOfRangeLevel(f"frame {t} outside [0, {self.iterations}]")
         if t in self._host_frames:
+            return self._host_frames[t]
+        if t in self._pending:
+            host, ev = self._pending.pop(t)
+            ev.synchronize()
+            self._host_frames[t] = host.numpy()
             return self._host_frames[t]
         from ._device import to_host64
         from .regularize import _device_iterate
