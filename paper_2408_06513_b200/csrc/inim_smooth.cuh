@@ -49,6 +49,37 @@ __device__ __forceinline__ void fir_line(const Taps& taps, int n, Load line, Sto
     }
 }
 
+// The same FIR with the input line read as float4 (inputs 4*q4 .. 4*q4 + 3): n is a
+// multiple of P, P a multiple of 4, and line4 may read up to 3 floats past the last
+// input (they are never used).
+template <int R, int P, typename Load4, typename Store>
+__device__ __forceinline__ void fir_line4(int n, Load4 line4, Store store) {
+    constexpr int NT = 2 * R + 1;
+    constexpr int NQ = P + NT - 1;
+    constexpr int NQ4 = (NQ + 3) / 4;
+    for (int p0 = 0; p0 < n; p0 += P) {
+        float acc[P];
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) acc[pp] = 0.f;
+#pragma unroll
+        for (int q4 = 0; q4 < NQ4; ++q4) {
+            const float4 v4 = line4((p0 >> 2) + q4);
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int q = 4 * q4 + e;
+#pragma unroll
+                for (int pp = 0; pp < P; ++pp) {
+                    const int t = q - pp;
+                    if (q < NQ && t >= 0 && t < NT) acc[pp] = fmaf(TapsOf<R / 3>::w(t), vv[e], acc[pp]);
+                }
+            }
+        }
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) store(p0 + pp, acc[pp]);
+    }
+}
+
 // ------------------------------------------------------------------------ horizontal
 // Tile: RH rows x TWH columns; lane = row, warp = a CW-wide column chunk.
 struct HGeo {
@@ -65,8 +96,18 @@ inline HGeo make_hgeo(int s) {
     return h;
 }
 
+// Row pitch of the staged input tile: at least TWH + 2R + 3 floats (the float4 reads
+// of fir_line4 run up to 3 past the line), a multiple of 4 with pitch/4 odd, so that
+// the 16-byte row stores and the 16-byte per-row FIR reads (lane = row) are both free
+// of bank conflicts.
+__host__ __device__ inline int h_pitch(const HGeo& h, int R) {
+    int p = (h.TWH + 2 * R + 3 + 3) & ~3;
+    if (((p >> 2) & 1) == 0) p += 4;
+    return p;
+}
+
 __host__ __device__ inline size_t h_smem_bytes(const HGeo& h, int R) {
-    return ((size_t)(h.TWH + 2 * R) * (h.RH + 1) + (size_t)h.RH * (h.TWH + 1)) * sizeof(float);
+    return ((size_t)h.RH * h_pitch(h, R) + (size_t)h.RH * (h.TWH + 1)) * sizeof(float);
 }
 
 // Horizontal pass of tile (bx, by).  zero_next (optional): the other count buffer of
@@ -75,9 +116,9 @@ template <int R, typename T>
 __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* __restrict__ out, int s, const HGeo& h,
                                               const Taps& taps, uint32_t* __restrict__ zero_next, int bx, int by,
                                               float* hsm) {
-    const int RH = h.RH, TWH = h.TWH, ld = RH + 1;
-    float* sh = hsm;                                 // [(TWH + 2R)][RH + 1]  transposed input
-    float* so = hsm + (size_t)(TWH + 2 * R) * ld;    // [RH][TWH + 1]          output staging
+    const int RH = h.RH, TWH = h.TWH, ld = h_pitch(h, R);
+    float* sh = hsm;                      // [RH][ld]         input rows (row-major)
+    float* so = hsm + (size_t)RH * ld;    // [RH][TWH + 1]    output staging
     const int j0 = by * RH, i0 = bx * TWH;
     const int W = TWH + 2 * R;
     const bool interior = i0 - R >= 0 && i0 + TWH + R <= s;
@@ -90,7 +131,7 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
     constexpr int NP4 = (128 + 2 * R + 127) / 128;  // 16-byte groups per lane per row (interior tiles)
     const bool vec = interior && (TWH & 3) == 0 && ((i0 - R) & 3) == 0 && (s & 3) == 0;
     for (int r0 = w; r0 < RH; r0 += RPW * nw) {
-        if (vec) {  // 16-byte loads of 4 consecutive columns, transposed into shared memory
+        if (vec) {  // 16-byte loads of 4 consecutive columns -> 16-byte row stores
             uint4 v4[RPW][NP4];
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {
@@ -110,16 +151,15 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
                 for (int e = 0; e < NP4; ++e) {
                     const int c = 4 * (lane + 32 * e);
                     if (r < RH && c < W) {
-                        // the four components go out in a lane-rotated order: with ld = RH + 1
-                        // lanes c4 and c4 + 8 share a bank for the same component, so lane
-                        // group (lane >> 3) starts at component (lane >> 3) (conflict-free)
                         const uint4 u = v4[q][e];
-#pragma unroll
-                        for (int kq = 0; kq < 4; ++kq) {
-                            const int comp = (kq + (lane >> 3)) & 3;
-                            const uint32_t bits = comp == 0 ? u.x : (comp == 1 ? u.y : (comp == 2 ? u.z : u.w));
-                            sh[(c + comp) * ld + r] = std::is_same<T, float>::value ? __uint_as_float(bits) : (float)bits;
+                        float4 f;
+                        if (std::is_same<T, float>::value) {
+                            f = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                                            __uint_as_float(u.w));
+                        } else {
+                            f = make_float4((float)u.x, (float)u.y, (float)u.z, (float)u.w);
                         }
+                        *reinterpret_cast<float4*>(sh + r * ld + c) = f;
                     }
                 }
             }
@@ -141,7 +181,7 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
 #pragma unroll
                 for (int e = 0; e < NPR; ++e) {
                     const int c = lane + 32 * e;
-                    if (r < RH && c < W) sh[c * ld + r] = (float)v[q][e];
+                    if (r < RH && c < W) sh[r * ld + c] = (float)v[q][e];
                 }
             }
         }
@@ -162,9 +202,13 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
     __syncthreads();
     if (lane < RH && w < h.NWH) {
         const int c0 = w * h.CW;
-        fir_line<R, 16>(
-            taps, h.CW, [&](int q) { return sh[(c0 + q) * ld + lane]; },
-            [&](int p, float v) { so[lane * (TWH + 1) + c0 + p] = v; });
+        const float* row = sh + lane * ld + c0;
+        auto store = [&](int p, float v) { so[lane * (TWH + 1) + c0 + p] = v; };
+        if ((h.CW & 15) == 0) {  // 16-byte reads of the row (c0 and ld are multiples of 4)
+            fir_line4<R, 16>(h.CW, [&](int q4) { return *reinterpret_cast<const float4*>(row + 4 * q4); }, store);
+        } else {
+            fir_line<R, 16>(taps, h.CW, [&](int q) { return row[q]; }, store);
+        }
     }
     __syncthreads();
     if ((TWH & 3) == 0) {  // 16-byte stores of the output tile
