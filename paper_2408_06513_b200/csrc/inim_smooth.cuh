@@ -226,6 +226,50 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
 }
 
 // -------------------------------------------------------------------------- vertical
+// Vertical FIR of one band's TH = 4P rows over TW columns by TW threads: thread t owns
+// the column quad (t % (TW/4)) and the row group (t / (TW/4)) of P output rows, reads
+// its P + 2R input rows as 16-byte loads (a warp reads whole 512-byte row segments),
+// keeps its 4P outputs in registers across a CTA barrier, then writes them in place over
+// the staged input (output row p of the CTA -> row p of `sh`): the tile needs no second
+// shared-memory buffer.  Every thread of the CTA calls it (`live` = owns a quad).
+template <int R, int P>
+__device__ __forceinline__ void fir_cols4_inplace(float* __restrict__ sh, int TW, int rb, int t, bool live,
+                                                  float background) {
+    constexpr int NT = 2 * R + 1;
+    const int nq = TW >> 2;
+    const int quad = t % nq, rg = t / nq;
+    const int r0 = rb + rg * P;
+    float4 acc[P];
+#pragma unroll
+    for (int pp = 0; pp < P; ++pp) acc[pp] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+#pragma unroll
+        for (int q = 0; q < P + NT - 1; ++q) {
+            const float4 v4 = *reinterpret_cast<const float4*>(sh + (r0 + q) * TW + 4 * quad);
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) {
+                const int tp = q - pp;
+                if (tp >= 0 && tp < NT) {
+                    const float w = TapsOf<R / 3>::w(tp);
+                    acc[pp].x = fmaf(w, v4.x, acc[pp].x);
+                    acc[pp].y = fmaf(w, v4.y, acc[pp].y);
+                    acc[pp].z = fmaf(w, v4.z, acc[pp].z);
+                    acc[pp].w = fmaf(w, v4.w, acc[pp].w);
+                }
+            }
+        }
+    }
+    __syncthreads();  // every input row has been read
+    if (live) {
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp)
+            *reinterpret_cast<float4*>(sh + (r0 + pp) * TW + 4 * quad) = make_float4(
+                acc[pp].x + background, acc[pp].y + background, acc[pp].z + background, acc[pp].w + background);
+    }
+}
+
+__host__ __device__ inline bool v_inplace(int TH, int TW, int GT) { return (TW & 3) == 0 && GT == TW && (TH == 32 || TH == 16); }
+
 struct VGeo {
     int VR, VB, GT;  // rows per CTA, bands per CTA, threads per band group
 };
@@ -239,6 +283,7 @@ inline VGeo make_vgeo(const Geo& g) {
 }
 
 __host__ __device__ inline size_t v_smem_bytes(const Geo& g, const VGeo& v, int R) {
+    if (v_inplace(g.TH, g.TW, v.GT)) return (size_t)(v.VR + 2 * R) * g.TW * sizeof(float);
     return ((size_t)(v.VR + 2 * R) * g.TW + (size_t)v.VR * g.TW) * sizeof(float);
 }
 
@@ -250,8 +295,9 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
                                               const VGeo& v, const Ws& ws, const Taps& taps, float background,
                                               int emit, int bx, int by, float* vsm) {
     const int TH = g.TH, TW = g.TW, s = g.s, VR = v.VR;
-    float* sh = vsm;                                 // [(VR + 2R)][TW]
-    float* sd = vsm + (size_t)(VR + 2 * R) * TW;     // [VR][TW]  d for VB bands
+    const bool inplace = v_inplace(TH, TW, v.GT);
+    float* sh = vsm;                                                 // [(VR + 2R)][TW]
+    float* sd = inplace ? vsm : vsm + (size_t)(VR + 2 * R) * TW;     // [VR][TW]  d for VB bands
     const int x = bx;
     const int a0 = by * VR, i0 = x * TW;
     const int H = VR + 2 * R;
@@ -287,7 +333,11 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     }
     __syncthreads();
     const int grp = threadIdx.x / v.GT, tid = threadIdx.x - grp * v.GT;
-    if (grp < v.VB && tid < TW) {
+    if (inplace) {  // (the branch is uniform over the CTA: it contains a barrier)
+        const bool live = grp < v.VB;
+        if (TH == 32) fir_cols4_inplace<R, 8>(sh, TW, grp * TH, tid, live, background);
+        else fir_cols4_inplace<R, 4>(sh, TW, grp * TH, tid, live, background);
+    } else if (grp < v.VB && tid < TW) {
         const int rb = grp * TH;  // first row of this group's band within the CTA
         fir_line<R, 8>(
             taps, TH, [&](int q) { return sh[(rb + q) * TW + tid]; },
