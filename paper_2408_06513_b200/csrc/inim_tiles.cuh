@@ -580,15 +580,15 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                     if (lane == 0 && i0 > 0) reinterpret_cast<float2*>(pd - 1)[1] = make_float2(res[0], res[1]);
                 }
             }
-            if (act && out.targets) {
+            if (act && out.targets) {  // default cache policy: the move gathers from it next
                 float* dst = out.targets + 2 * ((int64_t)j * s + i0 + u0);
                 if constexpr (CPL == 4) {
-                    __stcs(reinterpret_cast<float4*>(dst), make_float4(res[0], res[1], res[2], res[3]));
-                    __stcs(reinterpret_cast<float4*>(dst) + 1, make_float4(res[4], res[5], res[6], res[7]));
+                    reinterpret_cast<float4*>(dst)[0] = make_float4(res[0], res[1], res[2], res[3]);
+                    reinterpret_cast<float4*>(dst)[1] = make_float4(res[4], res[5], res[6], res[7]);
                 } else if constexpr (CPL == 2) {
-                    __stcs(reinterpret_cast<float4*>(dst), make_float4(res[0], res[1], res[2], res[3]));
+                    reinterpret_cast<float4*>(dst)[0] = make_float4(res[0], res[1], res[2], res[3]);
                 } else {
-                    __stcs(reinterpret_cast<float2*>(dst), make_float2(res[0], res[1]));
+                    reinterpret_cast<float2*>(dst)[0] = make_float2(res[0], res[1]);
                 }
             }
         }
