@@ -4,12 +4,14 @@
 // each a 6*ks+1-tap FIR with half-sample-symmetric reflection at the borders
 // (scipy.ndimage mode="reflect", period 2s).  The tile bodies live in inim_smooth.cuh
 // (shared with the persistent iteration kernel); these are the standalone launches.
+#include <type_traits>
+
 #include "inim_smooth.cuh"
 
 namespace inim {
 
 template <int R, typename T>
-__global__ void __launch_bounds__(256) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
+__global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
                                                        uint32_t* __restrict__ zero_next, uint32_t* ctr, int nctr) {
     pdl_enter();
