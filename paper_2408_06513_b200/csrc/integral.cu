@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* 
 // The write pass re-reads its tile straight from global memory (rows prefetched two
 // ahead in registers): no shared memory, so residency is bounded by registers only.
 template <int CPL, int MODE>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) write_kernel(const float* __restrict__ d, const Geo g,
+__global__ void __launch_bounds__(kWarpsPerCta * 32, CPL == 4 ? 5 : 1) write_kernel(const float* __restrict__ d, const Geo g,
                                                                   const Ws ws, const WriteOut out, const int* state) {
     pdl_enter();
     if (state && state[0]) return;  // displacement stop already reached
