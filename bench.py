@@ -268,8 +268,8 @@ def bench_ours(args):
     dom_bytes = algorithmic_bytes(dom, n, m)
     achieved = dom_bytes / (kernels[dom]["avg_us"] * 1e-6) / 1e9 if dom_bytes else None
 
-    # -- integral-image pass alone (BASELINE configs[4] at 4096^2), L2 flushed between reps
-    integral = bench_integral(lib, D, dev, flush, sizes=(12,), reps=10)
+    # -- integral-image pass alone (BASELINE configs[4] at 4096^2 and 16384^2), L2 flushed
+    integral = bench_integral(lib, D, dev, flush, sizes=(12, 14), reps=10)
 
     # -- end to end through the public API with host buffers (pinned), rank-local
     e2e = bench_e2e(P, host, k, reps=max(3, min(args.steps, 10)))
