@@ -454,3 +454,43 @@ def test_persistent_kernel_matches_graph_path(tmp_path):
     _lib.check(lib.inim_run_uncached(D.ptr(b), n, k, 8, 0.0, iters, 0.0, None, None, None, None, None,
                                      D.ptr(ws), D.stream()), "run")
     assert maxerr(np.load(tmp_path / "out.npy"), b.cpu().numpy()) <= 1e-6
+
+
+@pytest.mark.parametrize("k", [9, 12])
+def test_field_layouts_bit_identical(tmp_path, k):
+    """The move's paired (s, s, 4) and plain (s, s, 2) field layouts (INIM_PAIRS; paired
+    by default up to 2048^2, plain above) give bit-identical runs: same weights, same
+    blend order, only the gathers differ."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+
+    from conftest import ROOT
+
+    host = clusters(120_000, k).astype(np.float32)
+    np.save(tmp_path / "in.npy", host)
+    outs = []
+    for pairs in ("0", "1"):
+        dst = tmp_path / f"out{pairs}.npy"
+        script = textwrap.dedent(f"""
+            import sys
+            sys.path.insert(0, {str(ROOT)!r})
+            import numpy as np, torch
+            from paper_2408_06513_b200 import _device as D, _lib
+            lib = _lib.load()
+            host = np.load({str(tmp_path / "in.npy")!r})
+            n = len(host)
+            ws = torch.empty(int(lib.inim_workspace_bytes({k}, n)), dtype=torch.uint8, device="cuda")
+            a = torch.from_numpy(host).cuda()
+            _lib.check(lib.inim_run_uncached(D.ptr(a), n, {k}, 8, 0.0, 4, 0.0, None, None, None, None, None,
+                                             D.ptr(ws), D.stream()), "run")
+            np.save({str(dst)!r}, a.cpu().numpy())
+        """)
+        f = tmp_path / f"layout{pairs}.py"
+        f.write_text(script)
+        out = subprocess.run([sys.executable, str(f)], capture_output=True, text=True, timeout=300,
+                             env=dict(os.environ, INIM_PAIRS=pairs))
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(np.load(dst))
+    assert np.array_equal(outs[0], outs[1])
