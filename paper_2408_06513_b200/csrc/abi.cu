@@ -248,10 +248,11 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         if (rc) return rc;
         mp = &map;
     }
-    // once per run: both count buffers cleared (the smoothing of each iteration clears
-    // the reduce's band counters; the persistent kernel relies on this memset)
-    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * 2 * g.m, st));
-    INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, st));
+    // once per run: the first count buffer cleared (iteration 0's smoothing clears the
+    // other one for iteration 1); the persistent kernel needs both and its band counters
+    const bool mega_run = key.n > 0 && !key.fstats && use_mega(g, key.ks);
+    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (mega_run ? 2 : 1) * g.m, st));
+    if (mega_run) INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, st));
     prof_mark(st, "memset_counts");
     if (defect) {
         int rc = launch_flat_response(g.k, defect, st);
