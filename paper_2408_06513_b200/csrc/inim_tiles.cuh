@@ -438,6 +438,18 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
 #pragma unroll
     for (int e = 0; e < CPL; ++e) V[e] = UL[e] = UR[e] = 0.f;
     float exc = 0.f;
+    // the field's excursion max(0, -min, max - 1) (mapping.py:198-203) tracked as two
+    // running maxima, max(-gx, -gy) and max(gx, gy); max(g) - 1 == max(g - 1) exactly
+    float excHi = -1.f;
+    // per-column geometry of the field (hoisted out of the row sweep)
+    float colx[CPL], colb1[CPL], colip1[CPL];
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) {
+        const int i = i0 + u0 + e;
+        colx[e] = (float)i * scale;
+        colb1[e] = 2.f * colx[e] - 1.f;
+        colip1[e] = (float)(i + 1) * scale;
+    }
     // MODE 1 with an explicit defect: the row's values are fetched one row ahead so their
     // latency hides behind the previous row's work.
     const float2* defrow = (MODE == 2 && act)
@@ -537,12 +549,12 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
 #pragma unroll
             for (int e = 0; e < CPL; ++e) {
                 const int i = i0 + u0 + e;
-                const float xx = i * scale, b1 = 2.f * xx - 1.f;
+                const float xx = colx[e], b1 = colb1[e];
                 const float tl = (A[e] + Pr) + (off + loc[e]);
                 const float up = (UL[e] + UR[e] - V[e]) + (w1[e] + w2[e]);
                 float tln, upn;
                 if (diff) {
-                    tln = fmaf(tl, invCf, -((i + 1) * scale) * fj);
+                    tln = fmaf(tl, invCf, -colip1[e] * fj);
                     upn = fmaf(up, invCf, -(float)flat_up_count(i, s - 1 - i, j, tj1) * invs2f);
                 } else {
                     tln = tl * invCf;
@@ -561,7 +573,10 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                     gx -= dcur[e].x;
                     gy -= dcur[e].y;
                 }
-                if (act) exc = fmaxf(exc, fmaxf(fmaxf(-gx, -gy), fmaxf(gx - 1.f, gy - 1.f)));
+                if (act) {
+                    exc = fmaxf(exc, fmaxf(-gx, -gy));
+                    excHi = fmaxf(excHi, fmaxf(gx, gy));
+                }
                 res[2 * e] = __saturatef(gx);
                 res[2 * e + 1] = __saturatef(gy);
             }
@@ -604,6 +619,7 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
             if (r0 + q < TH) step(r0 + q, ring[q]);
     }
     if (MODE != 0) {
+        exc = fmaxf(exc, excHi - 1.f);
         exc = warp_max(exc);
         if (lane == 0 && exc > 0.f) atomic_max_nonneg(out.max_exc, exc);
     }
