@@ -502,7 +502,9 @@ def bench_splom(args):
                    "plots": cfg.nplots, "streams_per_gpu": cfg.streams,
                    "parallelism": f"plots sharded over {world} GPU(s), NCCL all-gather of final positions",
                    "l2": "flushed between timed steps"},
-        "gpu_launches": int(cfg.nplots * args.steps * (ITERS * 7 + 1)),
+        # per plot and run: 6 kernels per iteration, plus the first splat, the point sort
+        # (scan: 3 kernels, placement: 1) and the final unpermute
+        "gpu_launches": int(cfg.nplots * args.steps * (ITERS * job.lib.inim_kernels_per_iteration(cfg.k) + 6)),
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
