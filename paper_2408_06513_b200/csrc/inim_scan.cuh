@@ -175,7 +175,10 @@ __device__ __forceinline__ void chains_body(const Geo& g, const Ws& ws, int kk, 
     const int CH = (len + NY - 1) / NY;
     const int b0 = T.lo + min(len, ty * CH), b1 = T.lo + min(len, ty * CH + CH);  // [b0, b1)
     const int tb1 = min(b1, T.hi);  // step terms for b < hi
-    constexpr int U = 4;            // terms in flight per thread
+#ifndef INIM_CHAIN_U
+#define INIM_CHAIN_U 2  // measured: 2 beats 4 (+0.9% on the 16384^2 integral sweep) and 8
+#endif
+    constexpr int U = INIM_CHAIN_U;  // terms in flight per thread
     double loc = 0.0;
     {
         int b = b0;

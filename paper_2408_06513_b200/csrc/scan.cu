@@ -7,7 +7,12 @@
 
 namespace inim {
 
-__global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws, const int* state) {
+// INIM_CHAIN_MINB: experiment switch (measured: forcing 4 CTAs/SM = 32 registers spills
+// and is no faster than 3 CTAs/SM)
+#ifndef INIM_CHAIN_MINB
+#define INIM_CHAIN_MINB 1
+#endif
+__global__ void __launch_bounds__(512, INIM_CHAIN_MINB) chains_kernel(const Geo g, const Ws ws, const int* state) {
     pdl_enter();
     if (state && state[0]) return;
     __shared__ double part[16][33];
