@@ -36,6 +36,19 @@ def test_library_is_sm100a_only():
     assert archs == {"sm_100a"}, archs
 
 
+def test_chain_scan_keeps_three_ctas_per_sm():
+    """The standalone chain scan is occupancy-sensitive (72 registers =
+    1 CTA/SM cost 4% of the whole 16384^2 integral pass); 512 threads x <= 40 registers
+    keeps 3 CTAs/SM."""
+    from paper_2408_06513_b200 import _lib
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True, check=True).stdout.splitlines()
+    regs = [int(nxt.split("REG:")[1].split()[0]) for ln, nxt in zip(out, out[1:])
+            if "chains_kernel" in ln and "chains_reg" not in ln and "REG:" in nxt]
+    assert regs and max(regs) <= 40, regs
+
+
 def test_workspace_and_argument_errors_without_gpu():
     from paper_2408_06513_b200 import _lib
 
