@@ -41,7 +41,7 @@ extern "C" {
 #define INIM_EKERNEL (-3)     /* kernel_size < 1 (density.py:46-47) */
 #define INIM_EDRIVER (-4)     /* could not resolve cuTensorMapEncodeTiled */
 
-#define INIM_MAX_K 14 /* 16384^2: eight fp32 tables = 8 GiB */
+#define INIM_MAX_K 15 /* 32768^2 = 2^30 pixels (int32 pixel indices); eight fp32 tables = 32 GiB */
 
 /* Library identification: returns a static string, e.g. "libinim sm_100a 0.1". */
 const char* inim_version(void);
@@ -162,14 +162,6 @@ int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, in
 int inim_run_uncached(float* pts, int64_t n, int k, int kernel_size, float background, int iterations,
                       float stop_eps, float* frames, float* fields, float* disp, float* excursions, int* state,
                       void* ws, cudaStream_t stream);
-
-/* The persistent single-launch run (used by inim_run for 64^2..2048^2 grids with
- * kernel_size 8) with %globaltimer stamps written to stamps_dev (device, >= 16 u64) at
- * every phase boundary of the first iteration: splat, smooth_h, smooth_v+reduce,
- * band_rows, colscan, diagscan, marg, field, move.  Returns 1 if the persistent path
- * ran, 0 if this configuration uses the graph of standalone kernels, < 0 on error. */
-int inim_run_stamped(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, void* ws,
-                     cudaStream_t stream, unsigned long long* stamps_dev);
 
 /* Profiling: `iterations` iterations launched eagerly with a CUDA event recorded after
  * every launch; synchronises.  ms_out[q] = duration of launch q, names_out = the

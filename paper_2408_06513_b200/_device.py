@@ -23,6 +23,22 @@ def require_cuda():
     return _lib.load()
 
 
+MAX_K = 15  # include/inim.h INIM_MAX_K: 32768^2 = 2^30 pixels
+
+
+def check_grid(k: int) -> int:
+    """The device path covers grids up to 2^15 x 2^15 (int32 pixel indices; the eight fp32
+    tables alone take 32 GiB there).  The reference has no upper bound of its own but
+    allocates float64 (s, s) arrays, eight tables = 8 * 4^k * 8 bytes (256 GiB at k = 16):
+    past k = 15 it runs out of memory, and so does this path, with the same exception
+    type numpy raises."""
+    k = int(k)
+    if k > MAX_K:
+        raise MemoryError(f"a 2^{k} x 2^{k} grid exceeds the device path (k <= {MAX_K}); the reference's "
+                          f"float64 tables would need {8 * 8 * 4 ** k / 2 ** 30:.0f} GiB")
+    return k
+
+
 def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
@@ -40,6 +56,7 @@ def ptr(t) -> ctypes.c_void_p:
 def workspace(k: int, n: int = 0) -> torch.Tensor:
     """Grow-only per-device workspace for a 2^k grid and n points."""
     lib = require_cuda()
+    check_grid(k)
     need = int(lib.inim_workspace_bytes(int(k), int(n)))
     if need == 0:
         raise ValueError(f"k={k} out of range")

@@ -55,7 +55,6 @@ _SIGS = {
     "inim_run_uncached": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_float, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "inim_clear_graph_cache": (None, []),
-    "inim_run_stamped": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_void_p, c_void_p, c_void_p]),
     "inim_profile_run":(c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_void_p, c_void_p, c_void_p, c_int,
                                  ctypes.c_char_p, c_int]),
     "inim_run_host": (c_int, [c_void_p, c_void_p, c_i64, c_int, c_int, c_double, c_int]),
@@ -124,7 +123,7 @@ def check(rc: int, what: str):
     if rc == INIM_ENOTPOW2:
         raise ValueError("texture must be square with a power-of-two side")
     if rc == INIM_EKERNEL:
-        raise ValueError("kernel_size must be >= 1 (and <= 16 on the device path)")
+        raise ValueError("kernel_size must be >= 1")
     if rc == INIM_EDRIVER:
         raise InimError(f"{what}: could not resolve cuTensorMapEncodeTiled")
     raise InimError(f"{what}: CUDA error {rc}")

@@ -37,24 +37,6 @@ int launch_gather_points(const void* pts, int is_f64, const int64_t* rows, const
 int launch_trust(const double* orig, const double* moved, int64_t n, int nn, unsigned long long* out,
                  cudaStream_t st);
 int launch_order_pairs(const double* orig, const double* moved, int64_t n, unsigned long long* out, cudaStream_t st);
-bool mega_supported(const Geo& g, int kernel_size);
-int launch_mega(const Geo& g, const Ws& ws, int kernel_size, float bg, float eps, int iters, float* pts, float* pong,
-                int64_t n, uint32_t* counts, float* d, float* targets, const float* defect, float* frames,
-                float* fields, float* disp, float* excs, float* scratch, int* state, unsigned long long* stamps,
-                cudaStream_t st);
-
-// The persistent single-launch iteration (mega.cu) is opt-in (INIM_MEGA=1): measured
-// per phase it is not yet faster than the graph of standalone kernels, whose kernels
-// run at higher occupancy.
-static bool use_mega(const Geo& g, int ks) {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = getenv("INIM_MEGA");
-        env = (e && e[0] == '1') ? 1 : 0;
-    }
-    return env && !g_prof && mega_supported(g, ks);
-}
-static unsigned long long* g_stamps = nullptr;  // set by inim_run_stamped
 
 // Field layout the move gathers from: the paired layout (slot i = (t(i), t(i+1)), two
 // 16-byte gathers per point) while the field stays L2-resident, the plain (s, s, 2)
@@ -161,25 +143,12 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
         rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp);
         if (rc) return rc;
     }
-    // INIM_DUP=smooth|scan|field: enqueue that (idempotent) stage twice -- the graph's
-    // time difference is the stage's in-graph cost (timing experiments only)
-    static int dup = -1;
-    if (dup < 0) {
-        const char* e = getenv("INIM_DUP");
-        dup = !e ? 0 : (e[0] == 's' && e[1] == 'm') ? 1 : (e[0] == 's' && e[1] == 'c') ? 2 : (e[0] == 'f') ? 3 : 0;
-    }
-    for (int rep = 0; rep < (dup == 1 ? 2 : 1); ++rep) {
-        rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next);
-        if (rc) return rc;
-    }
-    for (int rep = 0; rep < (dup == 2 ? 2 : 1); ++rep) {
-        rc = launch_carry_scan_state(g, ws, flag, st);
-        if (rc) return rc;
-    }
-    for (int rep = 0; rep < (dup == 3 ? 2 : 1); ++rep) {
-        rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st, pairs);
-        if (rc) return rc;
-    }
+    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next);
+    if (rc) return rc;
+    rc = launch_carry_scan_state(g, ws, flag, st);
+    if (rc) return rc;
+    rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st, pairs);
+    if (rc) return rc;
     uint32_t* sn = chain.splat_next ? counts_next : nullptr;
     rc = pairs ? launch_sample_f32(pairs, g.k, pts_in, pts_out, n, 1, disp, flag, st, true, sn, chain.next_exc,
                                    chain.next_disp, chain.sorted)
@@ -249,10 +218,8 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         mp = &map;
     }
     // once per run: the first count buffer cleared (iteration 0's smoothing clears the
-    // other one for iteration 1); the persistent kernel needs both and its band counters
-    const bool mega_run = key.n > 0 && !key.fstats && use_mega(g, key.ks);
-    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * (mega_run ? 2 : 1) * g.m, st));
-    if (mega_run) INIM_CUDA_TRY(cudaMemsetAsync(w.bandctr, 0, sizeof(uint32_t) * g.B, st));
+    // other one for iteration 1)
+    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * g.m, st));
     prof_mark(st, "memset_counts");
     if (defect) {
         int rc = launch_flat_response(g.k, defect, st);
@@ -268,9 +235,6 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     const bool nb = fstats && key.orig_sub && nbstats && key.moved_sub && key.n_sub > 0;
     if (fstats) INIM_CUDA_TRY(cudaMemsetAsync(fstats, 0, sizeof(unsigned long long) * 3 * key.iters, st));
     if (nb) INIM_CUDA_TRY(cudaMemsetAsync(nbstats, 0, sizeof(unsigned long long) * 2 * key.iters, st));
-    if (key.n > 0 && !fstats && use_mega(g, key.ks))  // the whole run in one persistent launch
-        return launch_mega(g, w, key.ks, key.bg, key.eps, key.iters, pts, sortB, key.n, counts, d, tg_scratch, defect,
-                           frames, fields, disp, excursions, scratch, state, g_stamps, st);
     // Spatial order: for runs long enough to amortise it, the points are sorted by pixel
     // once (from the counts of iteration 0's splat, which the run needs anyway), the
     // moves then gather coalesced field rows and merge their splat atomics, and the
@@ -494,23 +458,6 @@ int inim_iterate(const float* pts_in, float* pts_out, int64_t n, int k, int kern
                              stream);
 }
 
-int inim_run_stamped(float* pts, int64_t n, int k, int kernel_size, float background, int iterations, void* ws,
-                     cudaStream_t stream, unsigned long long* stamps_dev) {
-    // The persistent path with %globaltimer stamps at every phase boundary of the first
-    // iteration (device buffer of >= 16 u64); returns 1 if the persistent path ran.
-    if (k < 1 || k > INIM_MAX_K || n <= 0 || iterations < 1 || !ws || !pts || !stamps_dev) return INIM_EINVAL;
-    const Geo g = make_geo(k);
-    if (!use_mega(g, kernel_size)) return 0;
-    RunKey key;
-    memset(&key, 0, sizeof(key));
-    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
-    key.iters = iterations;
-    g_stamps = stamps_dev;
-    const int rc = enqueue_run(key, pts, nullptr, nullptr, nullptr, nullptr, nullptr, ws, stream);
-    g_stamps = nullptr;
-    return rc ? rc : 1;
-}
-
 // Replay the cached executable graph of `key`, capturing it on first use.
 static int run_graph(const RunKey& key, float* pts, float* frames, float* fields, float* disp, float* excursions,
                      int* state, void* ws, cudaStream_t stream) {
@@ -519,10 +466,14 @@ static int run_graph(const RunKey& key, float* pts, float* frames, float* fields
         for (auto& e : g_cache)
             if (e.key == key) return (int)cudaGraphLaunch(e.exec, stream);
     }
-    // First call with these arguments: capture once (on a private stream: the legacy
-    // default stream cannot be captured), keep the executable graph, launch it on the
-    // caller's stream.
-    static cudaStream_t cap = nullptr;
+    // First call with these arguments: capture once (on a private stream of the current
+    // device: the legacy default stream cannot be captured), keep the executable graph,
+    // launch it on the caller's stream.
+    int dev = 0;
+    INIM_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDevices) return INIM_EINVAL;
+    static cudaStream_t caps[kMaxDevices] = {};
+    cudaStream_t& cap = caps[dev];
     if (!cap) INIM_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     cudaGraph_t graph;
     INIM_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
@@ -559,8 +510,6 @@ int inim_run(float* pts, int64_t n, int k, int kernel_size, float background, in
     key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
     key.iters = iterations; key.eps = stop_eps; key.frames = frames; key.fields = fields; key.disp = disp;
     key.exc = excursions; key.state = state; key.ws = ws; key.st = stream;
-    if (n > 0 && use_mega(make_geo(k), kernel_size))  // a handful of launches: no graph needed
-        return enqueue_run(key, pts, frames, fields, disp, excursions, state, ws, stream);
     return run_graph(key, pts, frames, fields, disp, excursions, state, ws, stream);
 }
 

@@ -153,6 +153,12 @@ __global__ void bg_gather_kernel(const float2* __restrict__ tg, const float* __r
     }
 }
 
+__host__ __device__ inline size_t edt_env_bytes(int s) {
+    return (((size_t)(s + 1) * sizeof(double) + (size_t)2 * s * sizeof(int)) + 255) & ~(size_t)255;
+}
+constexpr int kEdtSmemMaxK = 13;  // 16 * 8192 bytes = 128 KiB of shared memory
+constexpr int kEdtGlobalCtas = 296;
+
 // Column pass of the distance transform: nearest covered row per pixel (-1: none).
 __global__ void edt_cols_kernel(const uint8_t* __restrict__ covered, int k, int* __restrict__ nrow) {
     const int s = 1 << k;
@@ -173,13 +179,15 @@ __global__ void edt_cols_kernel(const uint8_t* __restrict__ covered, int k, int*
 }
 
 // Row pass: one warp per row; lane 0 builds the lower envelope of the column
-// parabolas in shared memory, then the warp fills the row's uncovered pixels from
-// their nearest covered pixel.
+// parabolas in shared memory (or, above 8192^2 where 16 s bytes exceed it, in a
+// per-CTA slice of global scratch `genv`), then the warp fills the row's uncovered
+// pixels from their nearest covered pixel.
 __global__ void edt_rows_fill_kernel(const uint8_t* __restrict__ covered, const int* __restrict__ nrow, int k,
-                                     double* __restrict__ out) {
+                                     double* __restrict__ out, unsigned char* genv) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int s = 1 << k;
-    double* z = reinterpret_cast<double*>(sm);        // s + 1 boundaries
+    unsigned char* env = genv ? genv + (size_t)blockIdx.x * edt_env_bytes(s) : sm;
+    double* z = reinterpret_cast<double*>(env);       // s + 1 boundaries
     int* v = reinterpret_cast<int*>(z + (s + 1));      // s apex columns
     int* best = v + s;                                 // s: nearest column per pixel
     const int lane = threadIdx.x;
@@ -231,6 +239,7 @@ struct BgScratch {
     uint32_t *counts, *offsets, *cursor, *cellof, *list, *bsum;
     uint8_t* covered;
     int* nrow;
+    unsigned char* env;  // k > kEdtSmemMaxK: per-CTA envelopes of the row pass
     size_t bytes;
 };
 
@@ -251,6 +260,7 @@ static BgScratch bg_layout(int k, void* base) {
     b.bsum = reinterpret_cast<uint32_t*>(take(4 * sort_bsum_words(k)));
     b.covered = reinterpret_cast<uint8_t*>(take(m));
     b.nrow = reinterpret_cast<int*>(take(4 * m));
+    b.env = k > kEdtSmemMaxK ? reinterpret_cast<unsigned char*>(take(kEdtGlobalCtas * edt_env_bytes(1 << k))) : nullptr;
     b.bytes = o;
     return b;
 }
@@ -268,13 +278,13 @@ using namespace inim;
 extern "C" {
 
 size_t inim_deform_background_scratch_bytes(int k) {
-    if (k < 1 || k > 13) return 0;
+    if (k < 1 || k > INIM_MAX_K) return 0;
     return bg_layout(k, nullptr).bytes;
 }
 
 int inim_deform_background(const float* targets, const float* values, int k, double* out, float* range2,
                            void* scratch, cudaStream_t stream) {
-    if (k < 1 || k > 13 || !targets || !values || !out || !range2 || !scratch) return INIM_EINVAL;
+    if (k < 1 || k > INIM_MAX_K || !targets || !values || !out || !range2 || !scratch) return INIM_EINVAL;
     const int s = 1 << k;
     const int64_t m = (int64_t)s * s;
     BgScratch b = bg_layout(k, scratch);
@@ -290,10 +300,14 @@ int inim_deform_background(const float* targets, const float* values, int k, dou
     bg_gather_kernel<<<grid_cap(m, 256), 256, 0, stream>>>(tg, values, k, b.offsets, b.counts, b.list, out,
                                                            b.covered);
     edt_cols_kernel<<<(s + 127) / 128, 128, 0, stream>>>(b.covered, k, b.nrow);
-    const size_t smem = (size_t)(s + 1) * sizeof(double) + (size_t)2 * s * sizeof(int);
-    if (smem > 48 * 1024)
-        INIM_CUDA_TRY(cudaFuncSetAttribute(edt_rows_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    edt_rows_fill_kernel<<<(unsigned)(s < 148 * 8 ? s : 148 * 8), 32, smem, stream>>>(b.covered, b.nrow, k, out);
+    if (b.env) {
+        edt_rows_fill_kernel<<<kEdtGlobalCtas, 32, 0, stream>>>(b.covered, b.nrow, k, out, b.env);
+    } else {
+        const size_t smem = (size_t)(s + 1) * sizeof(double) + (size_t)2 * s * sizeof(int);
+        if (smem > 48 * 1024) INIM_CUDA_TRY(ensure_smem_limit((const void*)edt_rows_fill_kernel, (int)smem));
+        edt_rows_fill_kernel<<<(unsigned)(s < 148 * 8 ? s : 148 * 8), 32, smem, stream>>>(b.covered, b.nrow, k, out,
+                                                                                        nullptr);
+    }
     return (int)cudaGetLastError();
 }
 

@@ -8,9 +8,30 @@
 
 #include <stdlib.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "inim_common.cuh"
 
 namespace inim {
+
+constexpr int kMaxDevices = 64;
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: raise a kernel's
+// limit once for every device it is launched on.
+inline cudaError_t ensure_smem_limit(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
+}
 
 struct Geo {
     int k, s, TH, TW, B, NX, NW, WL, CPL;  // WL = lanes holding columns; CPL = columns per lane
@@ -29,17 +50,6 @@ inline Geo make_geo(int k) {
     // one warp per tile: 64 columns (2 per lane) up to 2048^2 for more warps on small
     // grids, 128 columns (4 per lane, 16-byte accesses) above
     g.TW = g.s <= 2048 ? (g.s < 64 ? g.s : 64) : 128;
-    {  // geometry experiments: INIM_GEO_TH / INIM_GEO_TW override the large-grid choice
-        static int th = -1, tw = -1;
-        if (th < 0) {
-            const char* a = getenv("INIM_GEO_TH");
-            const char* b = getenv("INIM_GEO_TW");
-            th = a ? atoi(a) : 0;
-            tw = b ? atoi(b) : 0;
-        }
-        if (g.s >= 64 && th) g.TH = th;
-        if (g.s >= 64 && tw) g.TW = tw;
-    }
     g.CPL = g.TW >= 128 ? 4 : (g.TW >= 64 ? 2 : 1);
     g.B = g.s / g.TH;
     g.NX = g.s / g.TW;
@@ -68,7 +78,7 @@ struct WsLayout {
     size_t x2;       // float [B+1][s+TH]      URcar + TLcar[c-1], extended with TLcar[s-1]
     size_t hc;       // double [s][NX]         row prefix of d up to each tile's first column
     size_t rpre;     // double [s]             in-band inclusive prefix of the row totals
-    size_t bandctr;  // uint32 [B]             tiles reduced per band (self-resetting)
+    size_t taps;     // float [2s]             runtime taps of the generic smoothing (kernel_size > 16)
     size_t total;    // double [1]
     size_t misc;     // float [16]             scratch scalars
     size_t bytes;
@@ -101,7 +111,7 @@ inline WsLayout make_layout(const Geo& g) {
     L.x2 = take(sizeof(float) * (B + 1) * (s + TH));
     L.hc = take(sizeof(double) * s * NX);
     L.rpre = take(sizeof(double) * s);
-    L.bandctr = take(sizeof(uint32_t) * B);
+    L.taps = take(sizeof(float) * 2 * s);
     L.total = take(sizeof(double));
     L.misc = take(sizeof(float) * 16);
     L.bytes = o;
@@ -126,7 +136,7 @@ struct Ws {
     float* x2;
     double* hc;
     double* rpre;
-    uint32_t* bandctr;
+    float* taps;
     double* total;
     float* misc;
 };
@@ -150,7 +160,7 @@ inline Ws make_ws(void* base, const WsLayout& L) {
     w.x2 = reinterpret_cast<float*>(b + L.x2);
     w.hc = reinterpret_cast<double*>(b + L.hc);
     w.rpre = reinterpret_cast<double*>(b + L.rpre);
-    w.bandctr = reinterpret_cast<uint32_t*>(b + L.bandctr);
+    w.taps = reinterpret_cast<float*>(b + L.taps);
     w.total = reinterpret_cast<double*>(b + L.total);
     w.misc = reinterpret_cast<float*>(b + L.misc);
     return w;

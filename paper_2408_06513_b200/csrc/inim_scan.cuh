@@ -32,7 +32,7 @@
 
 namespace inim {
 
-constexpr int kMaxBands = 1024;  // s / TH for s = 16384, TH = 16
+constexpr int kMaxBands = 1024;  // s / TH: 16384 / 16 (k = 14) and 32768 / 32 (k = 15)
 
 // Block-wide exclusive scan of one double per thread.  *total receives the block total.
 __device__ __forceinline__ double block_excl_scan(double v, double* sh /* 33 */, double* total) {

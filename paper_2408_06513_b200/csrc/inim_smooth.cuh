@@ -1,6 +1,5 @@
 // Smoothing tile functions (gaussian_smooth + background, reference density.py:30-78),
-// shared by the standalone smoothing kernels (smooth.cu) and the persistent iteration
-// kernel (mega.cu).  Each function processes one tile with the whole CTA and contains
+// used by the smoothing kernels (smooth.cu).  Each function processes one tile with the whole CTA and contains
 // CTA-wide barriers, so every thread of the CTA must call it.
 #pragma once
 
@@ -288,8 +287,7 @@ __host__ __device__ inline size_t v_smem_bytes(const Geo& g, const VGeo& v, int 
 }
 
 // Vertical pass + background of tile (bx, by) = VB bands x TW columns; with `emit`,
-// each band's tile of d goes straight from shared memory into the tile reduce (emit = 2:
-// the band's last warp also computes the band lines, as the persistent kernel needs).
+// each band's tile of d goes straight from shared memory into the tile reduce.
 template <int R>
 __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, float* __restrict__ d, const Geo& g,
                                               const VGeo& v, const Ws& ws, const Taps& taps, float background,
@@ -345,21 +343,14 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     }
     __syncthreads();
     if (emit) {
-        // one warp per band tile of d, straight from shared memory; the reduce runs before
-        // this CTA stores d so its band-counter fence only waits on the aggregates
+        // one warp per band tile of d, straight from shared memory
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
         for (int gb = warp; gb < v.VB; gb += nwarps) {
             const float* src = sd + (size_t)gb * TH * TW;
             const int b = a0 / TH + gb;
-            if (emit == 2) {  // band lines by the band's last warp (the persistent kernel)
-                if (g.CPL == 4) warp_tile_reduce<4, true>(src, TW, g, ws, b, x, lane);
-                else if (g.CPL == 2) warp_tile_reduce<2, true>(src, TW, g, ws, b, x, lane);
-                else warp_tile_reduce<1, true>(src, TW, g, ws, b, x, lane);
-            } else {  // band lines by lines_kernel
-                if (g.CPL == 4) warp_tile_reduce<4, false>(src, TW, g, ws, b, x, lane);
-                else if (g.CPL == 2) warp_tile_reduce<2, false>(src, TW, g, ws, b, x, lane);
-                else warp_tile_reduce<1, false>(src, TW, g, ws, b, x, lane);
-            }
+            if (g.CPL == 4) warp_tile_reduce<4>(src, TW, g, ws, b, x, lane);
+            else if (g.CPL == 2) warp_tile_reduce<2>(src, TW, g, ws, b, x, lane);
+            else warp_tile_reduce<1>(src, TW, g, ws, b, x, lane);
         }
     }
     // the VR x TW tile of d out

@@ -83,41 +83,9 @@ __device__ __forceinline__ double warp_line_prefix(const T* src, double* __restr
     return carry;
 }
 
-// The lines of band b (run by the warp that reduced the band's last tile): for each row
-// j the exclusive prefix over tiles of the row sums (HC[j][x]) and the in-band inclusive
-// prefix of the row totals (rpre); the exclusive prefix over tiles of the tile totals
-// (tilepre) and the band total (btot).  Lane q walks row q serially (its loads issued
-// 16 at a time), so the whole band costs a few memory round trips.
-__device__ __forceinline__ void band_lines_warp(const Geo& g, const Ws& ws, int b, int lane) {
-    const int TH = g.TH, NX = g.NX, a = b * TH;
-    const double bt = warp_line_prefix(ws.tiletot + (int64_t)b * NX, ws.tilepre + (int64_t)b * NX, NX, lane);
-    if (lane == 0) ws.btot[b] = bt;
-    double rt = 0.0;
-    if (lane < TH) {
-        const float* rs = ws.rowsum + (int64_t)(a + lane) * NX;
-        double* hc = ws.hc + (int64_t)(a + lane) * NX;
-        constexpr int U = 16;
-        for (int x0 = 0; x0 < NX; x0 += U) {
-            float v[U];
-#pragma unroll
-            for (int q = 0; q < U; ++q) v[q] = x0 + q < NX ? __ldcg(rs + x0 + q) : 0.f;
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                if (x0 + q < NX) hc[x0 + q] = rt;
-                rt += (double)v[q];
-            }
-        }
-    }
-    const double inc = warp_inclusive_scan_d(rt, lane);
-    if (lane < TH) ws.rpre[a + lane] = inc;
-}
-
 // Per-tile aggregates of the reduce, fed one row at a time (lane l holds columns
 // CPL*l .. CPL*l + CPL - 1 of the row).  finish() writes inpre / tiletot / ulbot / urbot
-// / rowsum; with LINES it counts the band's reduced tiles and the warp that completes
-// the band runs band_lines_warp (threadfence-reduction pattern: no warp waits on
-// another).  The counters start at zero (cleared by the kernel before the reduce, or by
-// a memset) and are reset by the last warp.
+// / rowsum; the band lines are a launch of their own (lines_kernel).
 template <int CPL>
 struct TileReducer {
     const Geo& g;
@@ -166,7 +134,6 @@ struct TileReducer {
     __device__ __forceinline__ void set_rowsum(int r, float v) {
         if (lane == r) rs_mine = v;
     }
-    template <bool LINES>
     __device__ __forceinline__ void finish() {
         const int TH = g.TH, TW = g.TW, s = g.s, NX = g.NX;
         const int a = b * TH, i0 = x * TW, u0 = lane * CPL;
@@ -191,24 +158,13 @@ struct TileReducer {
         }
         if (lane == 31) ws.tiletot[(int64_t)b * NX + x] = linc;
         if (lane < TH) ws.rowsum[(int64_t)(a + lane) * NX + x] = rs_mine;
-        if (LINES) {
-            __threadfence();
-            unsigned old = 0;
-            if (lane == 0) old = atomicAdd(ws.bandctr + b, 1u);
-            old = __shfl_sync(kFull, old, 0);
-            if (old == (unsigned)(NX - 1)) {
-                __threadfence();
-                band_lines_warp(g, ws, b, lane);
-                if (lane == 0) ws.bandctr[b] = 0u;
-            }
-        }
     }
 };
 
 // The reduce of one tile from `src` (tile origin, row stride ld): a staged tile
 // (shared memory), or with GSRC global memory read through a ring of PF rows in flight
 // per lane, refilled as rows retire (PF = 8 measured slower than 2: registers).
-template <int CPL, bool LINES = true, bool GSRC = false>
+template <int CPL, bool GSRC = false>
 __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
                                                  int lane) {
     const int TH = g.TH;
@@ -244,7 +200,7 @@ __device__ __forceinline__ void warp_tile_reduce(const float* src, int ld, const
             red.row(r, dv);
         }
     }
-    red.template finish<LINES>();
+    red.finish();
 }
 
 // --------------------------------------------------------- flat response / anchors
@@ -310,12 +266,13 @@ INIM_DEV void slide_right(T (&w)[CPL], T ext, int r, int lane, int last) {  // i
     w[CPL - 1] = in;
 }
 
-// Region pixel counts of a constant s x s texture (exact; int32 is enough for k <= 14).
+// Region pixel counts of a constant s x s texture (exact).
 // wedge_up count: (j + 1) + g(min(j, i)) + g(min(j, s - 1 - i)),  g(L) = L (2j + 1 - L) / 2
-// (each L (2j + 1 - L) is even).  ri = s - 1 - i, tj1 = 2j + 1.
-INIM_DEV int flat_up_count(int i, int ri, int j, int tj1) {
-    const int l1 = min(j, i), l2 = min(j, ri);
-    return (j + 1) + ((l1 * (tj1 - l1) + l2 * (tj1 - l2)) >> 1);
+// (each L (2j + 1 - L) is even).  ri = s - 1 - i, tj1 = 2j + 1.  Each product is at
+// most j (j + 1) < s^2, so their sum fits uint32 up to s = 2^15 (INIM_MAX_K).
+INIM_DEV uint32_t flat_up_count(int i, int ri, int j, int tj1) {
+    const uint32_t l1 = (uint32_t)min(j, i), l2 = (uint32_t)min(j, ri), t = (uint32_t)tj1;
+    return (uint32_t)(j + 1) + ((l1 * (t - l1) + l2 * (t - l2)) >> 1);
 }
 INIM_DEV int64_t flat_apre_count(int sg, int s) {  // #{i' + j' <= sg}
     const int64_t S = s;

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_ring_kernel(const __
                 issue(kq + 2);
             }
         }
-        red.template finish<false>();  // band lines: lines_kernel
+        red.finish();  // band lines: lines_kernel
     }
 }
 
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* 
     const int tile = blockIdx.x * kWarpsPerCta + w;
     if (tile >= g.B * g.NX) return;
     const int b = tile / g.NX, x = tile - b * g.NX;
-    warp_tile_reduce<CPL, false, true>(d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW, g.s, g, ws, b, x, lane);
+    warp_tile_reduce<CPL, true>(d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW, g.s, g, ws, b, x, lane);
 }
 
 // The write pass re-reads its tile straight from global memory (rows prefetched two
@@ -236,23 +236,10 @@ static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const C
                              cudaStream_t st) {
     if (ring_map && g.TH % kChunk == 0 && g.TW >= 32) {
         const size_t smem = ring_smem_bytes(g);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(reduce_ring_kernel<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        static int per_sm = 0;
-        if (!per_sm) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reduce_ring_kernel<CPL>, kWarpsPerCta * 32, smem);
-            if (per_sm < 1) per_sm = 1;
-        }
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        INIM_CUDA_TRY(ensure_smem_limit((const void*)reduce_ring_kernel<CPL>, (int)smem));
         // one tile per warp: persistent warps (grid capped at residency, several tiles
         // per warp through the same ring) measured 2x slower at 16384^2
         const unsigned ctas = tile_ctas(g);
-        (void)sms;
         INIM_CUDA_TRY(launch_pdl(reduce_ring_kernel<CPL>, dim3(ctas), dim3(kWarpsPerCta * 32), smem, st, *ring_map, g,
                                  ws));
     } else {

@@ -1,4 +1,3 @@
-#include <cstdlib>
 // Point-stream kernels: the density splat (reference density.py:14-27 with pixel_of,
 // model.py:189-198) and the bilinear move (mapping.py:207-246 + the clip of
 // regularize.py:36).  Both stream the (n, 2) interleaved positions with 16-byte
@@ -443,15 +442,9 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
                       const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1,
                       bool sorted) {
     const int64_t npair = n >> 1;
-    static int u = 0;  // INIM_SAMPLE_U: pairs per thread per step (experiments)
-    if (!u) {
-        const char* e = getenv("INIM_SAMPLE_U");
-        u = e ? atoi(e) : 2;
-        if (u != 1 && u != 4) u = 2;
-    }
-    auto kern = u == 1 ? (pairs ? sample_f32_kernel<true, 1> : sample_f32_kernel<false, 1>)
-              : u == 4 ? (pairs ? sample_f32_kernel<true, 4> : sample_f32_kernel<false, 4>)
-                       : (pairs ? sample_f32_kernel<true, 2> : sample_f32_kernel<false, 2>);
+    // two point pairs (two 16-byte loads) per thread per step (measured: 1 or 4 are
+    // slower at C2)
+    auto kern = pairs ? sample_f32_kernel<true, 2> : sample_f32_kernel<false, 2>;
     INIM_CUDA_TRY(launch_pdl(kern, dim3(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256)), dim3(256), 0,
                              st, tg, k, reinterpret_cast<const float4*>(in), in, reinterpret_cast<float4*>(out), out, n,
                              clip, max_disp, state, splat_next, zn0, zn1, sorted ? 1 : 0));

@@ -13,11 +13,9 @@ namespace inim {
 template <int R, typename T>
 __global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
-                                                       uint32_t* __restrict__ zero_next, uint32_t* ctr, int nctr) {
+                                                       uint32_t* __restrict__ zero_next) {
     pdl_enter();
     if (state && state[0]) return;
-    if (ctr && blockIdx.x == 0 && blockIdx.y == 0)
-        for (int q = threadIdx.x; q < nctr; q += blockDim.x) ctr[q] = 0u;  // band counters of the reduce
     extern __shared__ __align__(16) float hsm[];
     smooth_h_tile<R, T>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
 }
@@ -30,6 +28,102 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
     smooth_v_tile<R>(tmp, d, g, v, ws, taps, background, emit, blockIdx.x, blockIdx.y, vsm);
+}
+
+// ------------------------------------------------------- generic taps (kernel_size > 16)
+// The compiled FIRs above carry the taps of kernel_size 1..16 as FFMA immediates.  Any
+// larger kernel (the reference accepts every kernel_size >= 1, density.py:40-51) runs
+// these runtime-tap kernels: the taps are evaluated on the device in float64 (the same
+// exp / sum as smoothing_kernel, the sum passed in from the host) and stored float32.
+// Reflection has period 2s, so when the kernel is longer than 2s its taps are folded
+// onto one period: tap t (offset t - R) adds into slot (t - R) mod 2s, and the pass
+// becomes a 2s-tap circular FIR with offsets 0..2s-1.
+//   nt taps, offset o0: out[p] = sum_{q < nt} taps[q] * line[reflect(p + o0 + q)]
+struct GenericTaps {
+    int R, nt, o0;
+    double sigma, inv_tot;
+};
+
+__global__ void generic_taps_kernel(float* __restrict__ taps, int s, const GenericTaps gt) {
+    pdl_enter();
+    const int64_t period = 2 * (int64_t)s;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < gt.nt; q += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        if (gt.o0 != 0) {  // unfolded: tap q is offset q - R
+            const double u = (double)(q - gt.R) / gt.sigma;
+            acc = exp(-0.5 * (u * u));
+        } else {  // folded: every offset o = q (mod 2s) in [-R, R]
+            int64_t o = (int64_t)q - ((int64_t)q + gt.R) / period * period;  // smallest o >= -R, o = q mod 2s
+            if (o < -gt.R) o += period;
+            for (; o <= gt.R; o += period) {
+                const double u = (double)o / gt.sigma;
+                acc += exp(-0.5 * (u * u));
+            }
+        }
+        taps[q] = (float)(acc * gt.inv_tot);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) generic_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
+                                                        const float* __restrict__ taps, const GenericTaps gt,
+                                                        const int* state, uint32_t* __restrict__ zero_next) {
+    pdl_enter();
+    if (state && state[0]) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= s) return;
+    const T* row = in + (int64_t)j * s;
+    float acc = 0.f;
+    for (int q = 0; q < gt.nt; ++q) acc = fmaf(__ldg(taps + q), (float)__ldg(row + reflect_index(i + gt.o0 + q, s)), acc);
+    out[(int64_t)j * s + i] = acc;
+    if (zero_next) zero_next[(int64_t)j * s + i] = 0u;
+}
+
+__global__ void __launch_bounds__(256) generic_v_kernel(const float* __restrict__ tmp, float* __restrict__ d, int s,
+                                                        const float* __restrict__ taps, const GenericTaps gt,
+                                                        float background, const int* state) {
+    pdl_enter();
+    if (state && state[0]) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
+    if (i >= s) return;
+    float acc = 0.f;
+    for (int q = 0; q < gt.nt; ++q)
+        acc = fmaf(__ldg(taps + q), __ldg(tmp + (int64_t)reflect_index(j + gt.o0 + q, s) * s + i), acc);
+    d[(int64_t)j * s + i] = acc + background;
+}
+
+static int launch_generic(const void* in, bool counts, const Geo& g, const Ws& ws, int kernel_size, float bg,
+                          float* d, bool emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
+    GenericTaps gt;
+    const int64_t R64 = 3 * (int64_t)kernel_size;
+    if (R64 > (int64_t)1 << 29) return INIM_EKERNEL;  // 6*ks+1 taps beyond int range
+    gt.R = (int)R64;
+    gt.sigma = kernel_size / 2.0;
+    {  // the normalisation of smoothing_kernel (density.py:30-37), float64 on the host
+        double tot = 0.0;
+        for (int t = -gt.R; t <= gt.R; ++t) {
+            const double u = t / gt.sigma;
+            tot += exp(-0.5 * (u * u));
+        }
+        gt.inv_tot = 1.0 / tot;
+    }
+    const bool fold = 2 * (int64_t)gt.R + 1 > 2 * (int64_t)g.s;
+    gt.nt = fold ? 2 * g.s : 2 * gt.R + 1;
+    gt.o0 = fold ? 0 : -gt.R;
+    INIM_CUDA_TRY(launch_pdl(generic_taps_kernel, dim3((gt.nt + 255) / 256), dim3(256), 0, st, ws.taps, g.s, gt));
+    const dim3 grid((g.s + 255) / 256, g.s), block(256);
+    if (counts)
+        INIM_CUDA_TRY(launch_pdl(generic_h_kernel<uint32_t>, grid, block, 0, st, static_cast<const uint32_t*>(in),
+                                 ws.tmp, g.s, (const float*)ws.taps, gt, state, zero_next));
+    else
+        INIM_CUDA_TRY(launch_pdl(generic_h_kernel<float>, grid, block, 0, st, static_cast<const float*>(in), ws.tmp,
+                                 g.s, (const float*)ws.taps, gt, state, zero_next));
+    prof_mark(st, "smooth_h");
+    INIM_CUDA_TRY(launch_pdl(generic_v_kernel, grid, block, 0, st, (const float*)ws.tmp, d, g.s,
+                             (const float*)ws.taps, gt, bg, state));
+    prof_mark(st, "smooth_v");
+    if (emit) return launch_reduce_from_global(d, g, ws, nullptr, st);  // the integral pass's tile aggregates
+    return (int)cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------- launch
@@ -49,17 +143,13 @@ void make_taps(int kernel_size, Taps* taps) {
 
 template <int R, typename T>
 static int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, uint32_t* zero_next,
-                    uint32_t* ctr, int nctr, cudaStream_t st) {
+                    cudaStream_t st) {
     const HGeo h = make_hgeo(s);
     const size_t smem = h_smem_bytes(h, R);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(smooth_h_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_h_kernel<R, T>, 200 * 1024));
     dim3 grid(s / h.TWH, s / h.RH);
     INIM_CUDA_TRY(launch_pdl(smooth_h_kernel<R, T>, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state,
-                             zero_next, ctr, nctr));
+                             zero_next));
     prof_mark(st, "smooth_h");
     return (int)cudaGetLastError();
 }
@@ -70,11 +160,7 @@ static int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, cons
 
     const VGeo v = make_vgeo(g);
     const size_t smem = v_smem_bytes(g, v, R);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(smooth_v_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
+    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_v_kernel<R>, 227 * 1024));
     dim3 grid(g.NX, g.s / v.VR);
     INIM_CUDA_TRY(launch_pdl(smooth_v_kernel<R>, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
                              state));
@@ -86,11 +172,8 @@ template <int KS>
 static int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
     constexpr int R = 3 * KS;
-    uint32_t* ctr = nullptr;  // the standalone reduce has no band counters (lines_kernel)
-    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next,
-                                            ctr, g.B, st)
-                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, ctr,
-                                         g.B, st);
+    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st)
+                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st);
     if (rc) return rc;
     return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st);
 }
@@ -98,7 +181,10 @@ static int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, 
 int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
                         float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
                         uint32_t* zero_next) {
-    if (kernel_size < 1 || 3 * kernel_size > kMaxR) return INIM_EKERNEL;  // 1 <= ks <= 16
+    if (kernel_size < 1) return INIM_EKERNEL;
+    if (3 * kernel_size > kMaxR)
+        return launch_generic(in, in_is_counts, g, ws, kernel_size, background, d, emit_aggregates, state, zero_next,
+                              st);
     Taps taps;
     make_taps(kernel_size, &taps);
     const int emit = emit_aggregates ? 1 : 0;

@@ -27,7 +27,7 @@ def _check_square_pow2(shape, what="grid"):
 def _splat_device(positions: np.ndarray, k: int) -> torch.Tensor:
     """Counts (s, s) int32 on the device; float64 coordinates binned in float64."""
     lib = D.require_cuda()
-    s = 1 << k
+    s = 1 << D.check_grid(k)
     counts = torch.zeros((s, s), dtype=torch.int32, device=D.device())
     pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 2)
     if len(pos):

@@ -146,7 +146,8 @@ def deform_background(run: RegularizationRun, upto: Optional[int] = None) -> Bac
     vrange = torch.empty(2, dtype=torch.float32, device=D.device())
     nbytes = int(lib.inim_deform_background_scratch_bytes(k))
     if nbytes == 0:
-        raise ValueError(f"deform_background supports k <= 13 on the device (k={k})")
+        D.check_grid(k)
+        raise ValueError(f"deform_background: k={k} out of range")
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=D.device())
     _lib.check(lib.inim_deform_background(D.ptr(targets), D.ptr(values), k, D.ptr(out), D.ptr(vrange),
                                              D.ptr(scratch), D.stream()), "deform_background")

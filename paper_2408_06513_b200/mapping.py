@@ -86,25 +86,38 @@ class _FlatResponseCache:
         self.builds = 0
 
     def _entry(self, k: int):
+        """The cache slot of k; creating it counts as one build (the arrays themselves
+        are materialised on first use: at k = 15 each is 16 GiB)."""
         if k not in self._cache:
-            lib = D.require_cuda()
-            s = 1 << k
-            dev64 = torch.empty((s, s, 2), dtype=torch.float64, device=D.device())
-            _lib.check(lib.inim_flat_response_f64(k, D.ptr(dev64), D.stream()), "flat_response")
-            self._cache[k] = {"host": dev64.cpu().numpy(), "dev64": dev64}
+            D.check_grid(k)
+            self._cache[k] = {"host": None, "dev64": None}
             self.builds += 1
         return self._cache[k]
 
     def get(self, k: int) -> np.ndarray:
-        return self._entry(k)["host"]
+        e = self._entry(k)
+        if e["host"] is None:
+            e["host"] = self.device64(k).cpu().numpy()
+        return e["host"]
 
     def is_flat(self, k: int, defect) -> bool:
         """True when `defect` is this cache's array for k (then the closed form is used)."""
         e = self._cache.get(k)
-        return e is not None and defect is e["host"]
+        return e is not None and e["host"] is not None and defect is e["host"]
 
     def device64(self, k: int):
-        return self._entry(k)["dev64"]
+        e = self._entry(k)
+        if e["dev64"] is None:
+            lib = D.require_cuda()
+            s = 1 << k
+            dev64 = torch.empty((s, s, 2), dtype=torch.float64, device=D.device())
+            _lib.check(lib.inim_flat_response_f64(k, D.ptr(dev64), D.stream()), "flat_response")
+            e["dev64"] = dev64
+        return e["dev64"]
+
+    def touch(self, k: int) -> None:
+        """Register the build of k without materialising it (regularize.run)."""
+        self._entry(k)
 
 
 flat_response = _FlatResponseCache()

@@ -296,7 +296,7 @@ class RegularizationRun:
             base = max(i for i in (0, *self._dev_frames) if i <= t)
             pos = self._device_frame(base)
             for _ in range(base, t):
-                pos = _device_iterate(pos, self.params)
+                pos, _ = _device_iterate(pos, self.params, with_field=False)
             arr = to_host64(pos)
         self._host_frames[t] = arr
         return arr

@@ -36,7 +36,7 @@ def iterate_once(positions: np.ndarray, params: RegularizationParams, defect: Op
     lib = D.require_cuda()
     density = build_density(positions, params)
     if defect is None:
-        defect = flat_response.get(params.k)
+        flat_response.touch(params.k)  # the closed form is evaluated in the field kernel
     k = params.k
     s = 1 << k
     dev_def = _defect_device(k, defect, torch.float32)
@@ -51,21 +51,25 @@ def iterate_once(positions: np.ndarray, params: RegularizationParams, defect: Op
     return new_positions, field, density
 
 
-def _device_iterate(pos: torch.Tensor, params: RegularizationParams) -> torch.Tensor:
-    """One float32 device iteration (the run loop's own step), used to recompute
-    frames thinned away by frame_cap.  Same kernels as inim_run: bit-identical."""
+def _device_iterate(pos: torch.Tensor, params: RegularizationParams, n: Optional[int] = None, with_field=True):
+    """One float32 device iteration (the run loop's own step): (new positions, field).
+    Used by stop="time" and to recompute frames thinned away by frame_cap.  Same kernels
+    as inim_run: bit-identical.  `n` (default: all rows of `pos`) may be 0 with a
+    one-row placeholder `pos`."""
     lib = D.require_cuda()
-    n = pos.shape[0]
+    if n is None:
+        n = pos.shape[0]
     k = params.k
-    s = 1 << k
     bufs = _run_buffers(n, k, 1, False)
     out = torch.empty_like(pos)
     bg = resolve_background(params, n)
     _lib.check(lib.inim_iterate(D.ptr(pos), D.ptr(out), n, k, params.kernel_size, bg, None, D.ptr(bufs["counts"]),
                                 D.ptr(bufs["d"]), D.ptr(bufs["targets"]), D.ptr(bufs["exc"]), D.ptr(bufs["disp"]),
                                 0.0, None, D.ptr(bufs["ws"]), D.stream()), "iterate")
-    del s
-    return out
+    if not with_field:
+        return out, None
+    field = DeformationField(k=k, max_excursion=float(bufs["exc"].item()), device_targets=bufs["targets"].clone())
+    return out, field
 
 
 _bufcache: dict = {}
@@ -74,6 +78,7 @@ _bufcache: dict = {}
 def _run_buffers(n: int, k: int, chunk: int, store_fields: bool):
     """Persistent device buffers per (n, k, chunk, store_fields): graph replays need
     stable pointers."""
+    D.check_grid(k)
     key = (torch.cuda.current_device(), n, k, chunk, store_fields)
     b = _bufcache.get(key)
     if b is None:
@@ -119,7 +124,8 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
     params.validate()
     lib = D.require_cuda()
     result = RegularizationRun(dataset, params, store_fields=store_fields)
-    flat_response.get(params.k)  # built once per run, as the reference (regularize.py:51)
+    flat_response.touch(params.k)  # built once per k, as the reference (regularize.py:51); the device
+    # iteration evaluates the closed form in registers, so the arrays stay unmaterialised
     n = dataset.n
     k = params.k
     bg = resolve_background(params, n)
@@ -142,6 +148,10 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
     state = b["state"]
     state.zero_()
     eps = float(params.epsilon) if params.stop == "displacement" else 0.0
+    if eps > 0.0:
+        # the device compares float32 displacements: a positive epsilon below the smallest
+        # float32 denormal must not round to 0 (which would disable the criterion)
+        eps = max(float(np.float32(eps)), float(np.finfo(np.float32).smallest_subnormal))
     keep = _survivors(params.iterations, params.frame_cap) if params.stop == "fixed" else None
     done = 0
     early = None
@@ -174,6 +184,8 @@ def run(dataset: ScatterDataset, params: RegularizationParams, collect_metrics: 
             st = state.cpu().numpy()
             executed = int(st[1]) - done
             stopped = bool(st[0])
+            if executed <= 0 and not stopped:
+                raise RuntimeError("run: the device executed no iteration of a displacement-stop chunk")
         else:
             executed, stopped = c, False
         excs = b["excs"][:executed].cpu().numpy() if executed and store_fields else []
@@ -216,11 +228,13 @@ def _run_timed(result: RegularizationRun, dataset: ScatterDataset, params: Regul
         if time.perf_counter() - started > params.time_budget:
             break
         tick = time.perf_counter()
-        new = _device_iterate(pos, params) if n else pos
+        new, field = _device_iterate(pos, params, n)
         torch.cuda.synchronize()
         wall = time.perf_counter() - tick
         result.wall_times.append(wall)
-        result._record(t, new)
+        if result.store_fields:
+            result.fields.append(field)
+        result._record(t, new if n else new[:0])
         if collect_metrics != "none":
             result.metrics.append(record_for_frame(t, dataset.positions, new if n else dataset.positions, params.k,
                                                    wall_ms=wall * 1e3, full=collect_metrics == "full",

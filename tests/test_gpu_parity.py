@@ -413,49 +413,6 @@ def test_larger_grids_run_against_oracle(P, oracle, k):
         assert maxerr(r.frame(t), frames[t]) <= POS_TOL, t
 
 
-def test_persistent_kernel_matches_graph_path(tmp_path):
-    """The opt-in persistent iteration kernel (INIM_MEGA=1, one cooperative launch for
-    the whole run) gives the same positions as the default kernel sequence."""
-    import os
-    import subprocess
-    import sys
-    import textwrap
-
-    import torch
-    from conftest import ROOT
-    from paper_2408_06513_b200 import _device as D, _lib
-
-    k, n, iters = 9, 60000, 4
-    host = clusters(n, 9).astype(np.float32)
-    np.save(tmp_path / "in.npy", host)
-    script = textwrap.dedent(f"""
-        import sys
-        sys.path.insert(0, {str(ROOT)!r})
-        import numpy as np, torch
-        from paper_2408_06513_b200 import _device as D, _lib
-        lib = _lib.load()
-        host = np.load({str(tmp_path / "in.npy")!r})
-        n = len(host)
-        ws = torch.empty(int(lib.inim_workspace_bytes({k}, n)), dtype=torch.uint8, device="cuda")
-        st = torch.zeros(16, dtype=torch.int64, device="cuda")
-        a = torch.from_numpy(host).cuda()
-        rc = lib.inim_run_stamped(D.ptr(a), n, {k}, 8, 0.0, {iters}, D.ptr(ws), D.stream(), D.ptr(st))
-        assert rc == 1, rc
-        np.save({str(tmp_path / "out.npy")!r}, a.cpu().numpy())
-    """)
-    f = tmp_path / "mega_check.py"
-    f.write_text(script)
-    env = dict(os.environ, INIM_MEGA="1")
-    out = subprocess.run([sys.executable, str(f)], capture_output=True, text=True, env=env, timeout=300)
-    assert out.returncode == 0, out.stderr[-2000:]
-    lib = _lib.load()
-    ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device="cuda")
-    b = torch.from_numpy(host).cuda()
-    _lib.check(lib.inim_run_uncached(D.ptr(b), n, k, 8, 0.0, iters, 0.0, None, None, None, None, None,
-                                     D.ptr(ws), D.stream()), "run")
-    assert maxerr(np.load(tmp_path / "out.npy"), b.cpu().numpy()) <= 1e-6
-
-
 @pytest.mark.parametrize("k", [9, 12])
 def test_field_layouts_bit_identical(tmp_path, k):
     """The move's paired (s, s, 4) and plain (s, s, 2) field layouts (INIM_PAIRS; paired
