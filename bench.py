@@ -2,20 +2,24 @@
 """Benchmark of the integral-image scatterplot regularizer (BASELINE.json metric:
 "regularization iters/sec (1M pts, 1024^2 grid); integral-image GB/s vs HBM peak").
 
-Workload (BASELINE.json configs[1], the paper's Fig. 5 case): 1,000,000 points in
+N = 1 (default): BASELINE configs[1], the paper's Fig. 5 case: 1,000,000 points in
 four Gaussian clusters (400k/300k/200k/100k, sigma 0.05, centres at 0.3/0.7),
 float32-representable, on a 1024^2 grid, kernel_size 8, 10 iterations.  One "step" is
 one full 10-iteration regularization of that input, device resident (inputs already in
-HBM).  L2 is flushed (256 MiB write) between timed steps.
+HBM).  L2 is flushed (256 MiB write) between timed steps.  The line also carries the
+integral-image pass (configs[4] at 4096^2 and 16384^2) and the SPLOM batch on this one
+GPU (configs[3], the N = 1 point of the scaling curve).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+N > 1: BASELINE configs[3], the SPLOM batch (256 plots x 500k points, 1024^2, 10
+iterations) sharded over N GPUs (strong scaling): each rank runs its block of plots as
+one batched run, and the step ends with one NCCL all-gather of every plot's final
+positions.  `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU).
 
-Under torchrun (N > 1) every rank regularizes its own plot (a SPLOM shard, weak
-scaling) and the final positions are all-gathered over NCCL inside the step; the
-step time is the max over ranks.
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload ...]
 
 `--impl reference` times the reference algorithm's CPU implementation (the C port in
-oracle/, all host threads) on the same workload; rank 0 only.
+oracle/, all host threads) on the same workload and config; rank 0 only.
 """
 
 from __future__ import annotations
@@ -183,6 +187,35 @@ def init_dist(world: int, backend: str):
     return dist
 
 
+SPLOM_POINTS = 500_000
+SPLOM_METRIC = "regularization iters/sec (SPLOM batch, 500k pts per plot, 1024² grid)"
+SPLOM_BYTES_PER_PLOT_ITER = 37.2e6  # 24 n + 24 m bytes at n = 500k, m = 1024^2
+
+
+def c2_config(world: int) -> dict:
+    """The config dict of the C2 line (identical in both arms)."""
+    return {"workload": "1M pts, 1024^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[1])",
+            "points": N_POINTS, "grid": 1 << K_GRID, "iterations_per_step": ITERS, "kernel_size": KERNEL_SIZE,
+            "input": "four_cluster(1M, seed=4)", "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single plot"}
+
+
+def c3_config(world: int) -> dict:
+    return {"workload": "16M pts, 4096^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[2])",
+            "points": 16_000_000, "grid": 4096, "iterations_per_step": ITERS, "kernel_size": KERNEL_SIZE,
+            "input": "c3_points(16M, seed=42)", "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": f"replicas x{world}" if world > 1 else "single plot"}
+
+
+def splom_config(world: int, plots: int) -> dict:
+    return {"workload": f"SPLOM {plots} plots x 500k pts, 1024^2, kernel_size 8, 10 iterations (BASELINE configs[3])",
+            "plots": plots, "points_per_plot": SPLOM_POINTS, "grid": 1 << K_GRID, "iterations_per_step": ITERS,
+            "kernel_size": KERNEL_SIZE, "input": "splom_plot(idx, 500k), PCG64 seeds (2408, idx)",
+            "parallelism": f"plots sharded over {world} GPU(s) (contiguous blocks), one batched run per rank, "
+                           "NCCL all-gather of the final positions inside the step",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
 # ------------------------------------------------------------------------ our arm
 def bench_ours(args):
     import torch
@@ -204,7 +237,7 @@ def bench_ours(args):
     m = 1 << (2 * k)
     pts_in = torch.from_numpy(host.astype(np.float32)).to(dev)
     pts = torch.empty_like(pts_in)
-    ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(lib.inim_workspace_bytes(k, n, 1)), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     gathered = torch.empty((world, n, 2), dtype=torch.float32, device=dev) if world > 1 else None
     stream = D.stream()
@@ -274,6 +307,13 @@ def bench_ours(args):
     # -- end to end through the public API with host buffers (pinned), rank-local
     e2e = bench_e2e(P, host, k, reps=max(3, min(args.steps, 10)))
 
+    # -- the SPLOM batch (configs[3]) on this GPU: the N = 1 point of the scaling curve
+    splom = None
+    if world == 1 and not args.no_splom and args.workload in (None, "c2"):
+        splom = bench_splom(args, emit=False)
+        for key in ("config", "data", "clocks", "vs_baseline", "higher_is_better", "dtype"):
+            splom.pop(key, None)
+
     if rank != 0:
         return
     cpu = cpu_baseline(host, k, iterations=4 if k == K_GRID else 2) \
@@ -293,12 +333,7 @@ def bench_ours(args):
         "dtype": "f32",
         "data": ("synthetic gaussian mixture (4-8 clusters, sigma 0.02-0.06), fp32-representable" if c3 else
                  "synthetic four-cluster (400k/300k/200k/100k, sigma 0.05), fp32-representable"),
-        "config": {"workload": ("16M pts, 4096^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[2])"
-                                if c3 else
-                                "1M pts, 1024^2 grid, kernel_size 8, 10 iterations per step (BASELINE configs[1])"),
-                   "points": n, "grid": 1 << k, "iterations_per_step": ITERS, "kernel_size": KERNEL_SIZE,
-                   "l2": "flushed between timed steps (256 MiB write)",
-                   "parallelism": f"splom-shard x{world}" if world > 1 else "single plot"},
+        "config": c3_config(world) if c3 else c2_config(world),
         "e2e": e2e,
         "gpu_launches": int(args.steps * sum(v["launches_per_step"] for nm, v in kernels.items()
                                              if nm != "memset_counts")),
@@ -314,6 +349,7 @@ def bench_ours(args):
         "integral_image": integral,
         "cpu_baseline": cpu,
         "clocks": clocks,
+        "splom_1gpu": splom,
     }
     print(json.dumps(line), flush=True)
 
@@ -332,7 +368,7 @@ def bench_integral(lib, D, dev, flush, sizes=(12,), reps=10):
         d = torch.rand((s, s), generator=g, device=dev, dtype=torch.float32) * 10.0
         tables = torch.empty((8, s, s), dtype=torch.float32, device=dev)
         total = torch.empty(1, dtype=torch.float64, device=dev)
-        ws = torch.empty(int(lib.inim_workspace_bytes(k, 0)), dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(lib.inim_workspace_bytes(k, 0, 1)), dtype=torch.uint8, device=dev)
         st = D.stream()
 
         def once():
@@ -409,72 +445,138 @@ def cpu_baseline(host: np.ndarray, k: int = K_GRID, iterations: int = 4):
                       f"port of the reference algorithm, OpenMP {cores} threads)"}
 
 
-def bench_reference(args):
+def bench_reference(args, workload: str):
+    """The reference arm: the reference algorithm's CPU implementation (the C port in
+    oracle/, every host thread) on our arm's workload, config, metric and unit; each
+    step is a bounded sample of that workload.  Rank 0 only."""
     rank, world, _local = dist_env()
     if rank != 0:
         return
     from oracle import oracle as O
 
-    host = four_cluster(N_POINTS, seed=4)
     cores = os.cpu_count() or 1
     O.set_threads(cores)
     defect = O.flat_response(K_GRID)
-    pos = host
-    for _ in range(args.warmup):
-        pos = O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
-    pos = host
+    if workload == "splom":
+        from paper_2408_06513_b200.splom import splom_plot
+
+        plots = [splom_plot(i, SPLOM_POINTS) for i in range(2)]
+        metric, unit, config = SPLOM_METRIC, "plot-iters/s", splom_config(world, args.plots)
+        sample = (f"each step = 1 iteration of one 500k-point / 1024^2 / ks=8 SPLOM plot (plots 0 and 1 "
+                  f"alternating); float64 C port of the reference algorithm, OpenMP {cores} threads")
+
+        def step(q, pos):
+            return O.iterate_once(pos[q % 2], K_GRID, KERNEL_SIZE, None, defect)
+
+        state = plots
+    else:
+        host = four_cluster(N_POINTS, seed=4)
+        metric, unit, config = METRIC, "iters/s", c2_config(world)
+        sample = (f"each step = 1 iteration of the 1M-point / 1024^2 / ks=8 workload (the timed unit of our arm is "
+                  f"10 iterations); float64 C port of the reference algorithm, OpenMP {cores} threads")
+
+        def step(q, pos):
+            return O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
+
+        state = host
+    for q in range(args.warmup):
+        out = step(q, state)
+        if workload != "splom":
+            state = out
+    state = plots if workload == "splom" else host
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        pos = O.iterate_once(pos, K_GRID, KERNEL_SIZE, None, defect)
+    for q in range(args.steps):
+        out = step(q, state)
+        if workload != "splom":
+            state = out
     dt = time.perf_counter() - t0
     value = args.steps / dt
-    sample = (f"each step = 1 iteration of the 1M-point / 1024^2 / ks=8 workload (the timed unit of our arm is "
-              f"10 iterations); float64 C port of the reference algorithm, OpenMP {cores} threads")
     line = {
-        "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic four-cluster, fp32-representable",
-        "config": {"workload": "1M pts, 1024^2 grid, kernel_size 8 (BASELINE configs[1])", "points": len(host),
-                   "grid": 1 << K_GRID},
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if workload == "splom" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, fp32-representable (same generators as our arm)", "config": config,
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def bench_splom(args):
+class _StubSplom:
+    """CPU stand-in for DeviceSplom (--cpu-stub): the same shard / run / gather plumbing
+    with the per-plot compute replaced by a deterministic transform, so the multi-rank
+    path of this file runs on gloo without a GPU (tests/test_distributed.py)."""
+
+    def __init__(self, ids, points):
+        import torch
+
+        self.ids = list(ids)
+        self.work = torch.zeros((len(self.ids), points, 2), dtype=torch.float32)
+
+    def run(self):
+        for q, idx in enumerate(self.ids):
+            self.work[q].fill_(float(idx))
+        return self.work
+
+
+def splom_job(args, world: int, rank: int, device_stub: bool):
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, shard, splom_plot
+
+    ids = shard(args.plots, world, rank)
+    points = args.splom_points
+    if device_stub:
+        return _StubSplom(ids, points), ids
+    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS)
+    job = DeviceSplom(cfg, ids)
+    job.load(lambda i: splom_plot(i, points))
+    return job, ids
+
+
+def bench_splom(args, emit: bool = True):
     """BASELINE configs[3]: SPLOM of --plots plots x 500k points, 1024^2, 10 iterations,
-    plots sharded over ranks, concurrent streams per GPU, one NCCL all-gather of the
-    final positions inside the step.  value = plot-iterations per second (whole job)."""
+    plots sharded over ranks (one batched run per rank), one NCCL all-gather of the
+    final positions inside the step.  value = plot-iterations per second (whole job),
+    time = max over ranks of the device-timed steps.  With emit=False (the N = 1 C2
+    line) returns the measurement instead of printing it."""
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dist = init_dist(world, "nccl")
-    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, gather_results, shard, splom_plot
+    stub = args.cpu_stub
+    if not stub:
+        torch.cuda.set_device(local)
+    dist = init_dist(world, "gloo" if stub else "nccl")
+    from paper_2408_06513_b200.splom import gather_results
 
-    cfg = SplomConfig(nplots=args.plots, points=500_000, k=10, kernel_size=8, iterations=ITERS, streams=8)
-    ids = shard(cfg.nplots, world, rank)
-    job = DeviceSplom(cfg, ids)
-    job.load(lambda i: splom_plot(i, cfg.points))
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    job, ids = splom_job(args, world, rank, stub)
+    flush = None if stub else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    gathered = {}
 
     def step():
         res = job.run()
-        if world > 1:
-            gather_results(res, cfg.nplots, world)
+        gathered["all"] = gather_results(res, args.plots, world) if world > 1 else res
+
+    def sync():
+        if not stub:
+            torch.cuda.synchronize()
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
+    sync()
+    sampler = None
+    if not stub:
+        sampler = ClockSampler(local)
+        sampler.start()
     if world > 1:
         dist.barrier()
-    torch.cuda.synchronize()
+    sync()
     t_ms = 0.0
     for _ in range(args.steps):
+        if stub:
+            t0 = time.perf_counter()
+            step()
+            t_ms += (time.perf_counter() - t0) * 1e3
+            continue
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -482,32 +584,94 @@ def bench_splom(args):
         b.record()
         b.synchronize()
         t_ms += a.elapsed_time(b)
+    sync()
     if world > 1:
         dist.barrier()
-    clocks = sampler.summary()
+    clocks = sampler.summary() if sampler else None
     if world > 1:
-        t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([t_ms], dtype=torch.float64, device="cpu" if stub else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
-    if rank != 0:
-        return
-    total_iters = cfg.nplots * ITERS * args.steps
+    allres = gathered["all"]
+    gather_ok = bool(allres.shape[0] == args.plots)
+    if stub:  # every plot's block came back in order
+        gather_ok = gather_ok and all(float(allres[i, 0, 0]) == float(i) for i in range(args.plots))
+    e2e = None if stub else splom_e2e(args, job, world, dist)
+    total_iters = args.plots * ITERS * args.steps
     value = total_iters / (t_ms / 1e3)
-    line = {
-        "metric": "regularization iters/sec (SPLOM batch, 500k pts per plot, 1024² grid)",
-        "value": value, "unit": "plot-iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic gaussian mixtures (PCG64 seeds (2408, plot))",
-        "config": {"workload": f"SPLOM {cfg.nplots} plots x 500k pts, 1024^2, 10 iterations (BASELINE configs[3])",
-                   "plots": cfg.nplots, "streams_per_gpu": cfg.streams,
-                   "parallelism": f"plots sharded over {world} GPU(s), NCCL all-gather of final positions",
-                   "l2": "flushed between timed steps"},
-        # per plot and run: 6 kernels per iteration, plus the first splat, the point sort
-        # (scan: 3 kernels, placement: 1) and the final unpermute
-        "gpu_launches": int(cfg.nplots * args.steps * (ITERS * job.lib.inim_kernels_per_iteration(cfg.k) + 6)),
+    peaks = measured_peaks()
+    achieved = SPLOM_BYTES_PER_PLOT_ITER * value / 1e9
+    launches = None if stub else int(args.steps * job_launches(job))
+    out = {
+        "metric": SPLOM_METRIC, "value": value, "unit": "plot-iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": ("CPU stub (per-plot compute replaced; plumbing test only)" if stub else
+                 "synthetic gaussian mixtures (PCG64 seeds (2408, plot)), fp32-representable"),
+        "config": splom_config(world, args.plots),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "whole iteration (all stages, batched)", "achieved": achieved,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                     "traffic": None, "peak_source": peaks["source"],
+                     "algorithmic_bytes_per_plot_iteration": SPLOM_BYTES_PER_PLOT_ITER,
+                     "method": "24 n + 24 m bytes per plot-iteration (SURVEY 8(d)) x plot-iterations / s"},
+        "collective": {"backend": dist.get_backend() if world > 1 else None, "world": world,
+                       "op": "all_gather_into_tensor of final positions" if world > 1 else None,
+                       "bytes_per_step": int(args.plots * args.splom_points * 8) if world > 1 else 0,
+                       "gather_ok": gather_ok},
+        "plots_per_rank": len(ids),
         "clocks": clocks,
     }
-    print(json.dumps(line), flush=True)
+    if not emit:
+        return out
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    return out
+
+
+def job_launches(job) -> int:
+    """Kernels per SPLOM step: per batched run, the splat, the point sort (3 scan kernels
+    + placement), six kernels per iteration and the final unpermute (+ the counts
+    memset node, not a kernel)."""
+    runs = -(-len(job.ids) // job.batch)
+    return runs * (1 + 4 + 6 * ITERS + 1)
+
+
+def splom_e2e(args, job, world, dist):
+    """The same step through the public API with host buffers: every rank copies its
+    block of plots from pinned host memory (float32, as the batch API takes them),
+    runs it, and copies its block of final positions back; time = max over ranks."""
+    import torch
+
+    host_in = torch.empty(tuple(job.inputs.shape), dtype=torch.float32).pin_memory()
+    host_in.copy_(job.inputs.cpu())
+    host_out = torch.empty_like(host_in).pin_memory()
+
+    def call():
+        job.inputs.copy_(host_in, non_blocking=True)
+        res = job.run()
+        host_out.copy_(res, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(2):
+        call()
+    times = []
+    for _ in range(max(3, min(args.steps, 5))):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    if world > 1:
+        t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    nbytes = int(host_in.numel() * 4)
+    return {"value": args.plots * ITERS / dt, "unit": "plot-iters/s", "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "ms_per_call": dt * 1e3, "statistic": "median wall time, max over ranks",
+            "api": "DeviceSplom.run (inim_run_batched) with pinned float32 host buffers, each rank its own block"}
 
 
 def bench_sweep(args):
@@ -535,29 +699,61 @@ def bench_sweep(args):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: run this file under torch.distributed.run with N
+    ranks (one per GPU) and pass its exit code through."""
+    import subprocess
+
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL prints nranks per communicator: the rank count is on record
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "splom", "sweep"],
-                    help="c2: 1M pts/1024^2 (headline); c3: 16M pts/4096^2; splom: configs[3]; "
-                         "sweep: integral-only 512^2..16384^2")
+    ap.add_argument("--workload", default=None, choices=["c2", "c3", "splom", "sweep"],
+                    help="default: c2 (1M pts/1024^2, the headline) on one GPU, splom (configs[3]) on N > 1; "
+                         "c3: 16M pts/4096^2; sweep: integral-only 512^2..16384^2")
     ap.add_argument("--plots", type=int, default=256)
+    ap.add_argument("--splom-points", type=int, default=SPLOM_POINTS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-splom", action="store_true", help="N = 1: leave the SPLOM batch out of the C2 line")
+    ap.add_argument("--cpu-stub", action="store_true", help="multi-rank plumbing on gloo, no GPU (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    workload = args.workload or ("c2" if world == 1 else "splom")
     if args.impl == "reference":
-        bench_reference(args)
-    elif args.workload == "splom":
+        bench_reference(args, workload)
+    elif args.cpu_stub:
         bench_splom(args)
-    elif args.workload == "sweep":
+    elif workload == "splom":
+        bench_splom(args)
+    elif workload == "sweep":
         bench_sweep(args)
     else:
         bench_ours(args)
-    _rank, world, _ = dist_env()
     if world > 1:
         import torch.distributed as dist
 

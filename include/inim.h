@@ -48,10 +48,11 @@ const char* inim_version(void);
 
 /* Bytes of device workspace needed by the calls below for a 2^k grid and n points
  * (integral aggregates and carries, the smoothing scratch, and for inim_run the
- * counts / density / field buffers plus a point ping-pong buffer of n*2 floats).
+ * counts / density / field buffers plus a point ping-pong buffer of n*2 floats), for
+ * B plots (inim_run_batched: B slabs of the single-plot size; B <= 1 means one).
  * `ws` arguments must be at least this large and 256-byte aligned.  0 if k is out of
  * range. */
-size_t inim_workspace_bytes(int k, int64_t n);
+size_t inim_workspace_bytes(int k, int64_t n, int B);
 
 /* accumulate (density.py:14-27) + pixel_of (model.py:189-198): counts[j*s+i] += number
  * of points in pixel (i, j).  Integer atomics: bit-exact for identical coordinates.
@@ -187,6 +188,18 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
                      float* frames, float* fields, float* disp, float* excursions, int* state, void* ws,
                      cudaStream_t stream, unsigned long long* frame_stats, const double* orig_sub, const int64_t* pick,
                      int64_t n_sub, int n_neighbors, double* moved_sub, unsigned long long* nb_stats);
+
+/* A batch of B independent plots of n points each (a scatterplot matrix; the reference
+ * runs regularize.run per plot in a process pool, tests/test_acceptance.py:107-128):
+ * `iterations` fixed iterations of every plot, every stage ONE launch over all plots
+ * (plot index in grid.z), captured once into a CUDA graph and replayed.
+ * pts: device (B, n, 2) float32, updated in place to each plot's final positions (n
+ * even when B > 1); ws: inim_workspace_bytes(k, n, B) bytes.  frame_stats: NULL, or
+ * device u64[B][iterations][3] (cleared by the call) receiving the per-frame occupancy
+ * statistics of every plot (as inim_run_metrics; collect_metrics="basic").  The result
+ * of each plot is bit-identical to inim_run on that plot alone. */
+int inim_run_batched(float* pts, int64_t n, int B, int k, int kernel_size, float background, int iterations,
+                     unsigned long long* frame_stats, void* ws, cudaStream_t stream);
 
 /* Occupancy statistics of a count grid (binned_stddev metrics.py:46-59, overplotting
  * metrics.py:62-71): out3 (device u64[3], NOT cleared) += {occupied pixels, sum over the

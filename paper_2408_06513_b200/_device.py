@@ -57,7 +57,7 @@ def workspace(k: int, n: int = 0) -> torch.Tensor:
     """Grow-only per-device workspace for a 2^k grid and n points."""
     lib = require_cuda()
     check_grid(k)
-    need = int(lib.inim_workspace_bytes(int(k), int(n)))
+    need = int(lib.inim_workspace_bytes(int(k), int(n), 1))
     if need == 0:
         raise ValueError(f"k={k} out of range")
     key = torch.cuda.current_device()

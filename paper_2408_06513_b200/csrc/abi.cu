@@ -11,27 +11,29 @@
 
 namespace inim {
 int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st,
-                     float* zero0 = nullptr, float* zero1 = nullptr);
+                     float* zero0 = nullptr, float* zero1 = nullptr, const Bat& bt = Bat{});
 int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cudaStream_t st);
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
                       const int* state, cudaStream_t st, bool pairs = false, uint32_t* splat_next = nullptr,
-                      float* zn0 = nullptr, float* zn1 = nullptr, bool sorted = false);
+                      float* zn0 = nullptr, float* zn1 = nullptr, bool sorted = false, const Bat& bt = Bat{},
+                      int64_t zin = 0, int64_t zout = 0);
 int launch_sample_f64(const float* tg, int k, const double* in, double* out, int64_t n, int clip, cudaStream_t st);
 int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_t st);
 int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st);
-int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st);
 int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
                         float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
-                        uint32_t* zero_next = nullptr);
+                        uint32_t* zero_next = nullptr, const Bat& bt = Bat{});
 int launch_field_from_tables(const float* t8, int k, const double* total, const float* defect, float* targets,
                              float* max_exc, cudaStream_t st);
 int launch_flat_response(int k, float* defect, cudaStream_t st);
 int launch_line_scan(const float* in, float* out, int s, int dj, int di, int exclusive, cudaStream_t st);
 size_t sort_bsum_words(int k);
 int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* counts, uint32_t* cursor,
-                       uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st);
-int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st);
-int launch_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t st);
+                       uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st, const Bat& bt = Bat{});
+int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st,
+                     const Bat& bt = Bat{});
+int launch_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t st,
+                       const Bat& bt = Bat{}, int64_t zout = 0);
 int launch_gather_points(const void* pts, int is_f64, const int64_t* rows, const uint32_t* perm, int64_t m,
                          double* out, cudaStream_t st);
 int launch_trust(const double* orig, const double* moved, int64_t n, int nn, unsigned long long* out,
@@ -131,29 +133,31 @@ struct Chain {
 // One iteration.  `counts` must be zero on entry (or already filled, chain.splatted);
 // `counts_next` (optional) is cleared by the smoothing pass for the next iteration.
 // With `pairs` the field is (also) written in the paired layout and the move reads
-// that; `targets` may then be null.
+// that; `targets` may then be null.  `bt`: a batch of plots (grid.z), with zin / zout
+// the plot strides (floats) of pts_in / pts_out.
 static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, const Geo& g, int kernel_size,
                              float background, const float* defect, uint32_t* counts, uint32_t* counts_next, float* d,
                              float* targets, float* max_exc, float* disp, float stop_eps, int* state, const Ws& ws,
                              const CUtensorMap* map, cudaStream_t st, float* pairs = nullptr,
-                             const Chain& chain = Chain{false, false, nullptr, nullptr, false}) {
+                             const Chain& chain = Chain{false, false, nullptr, nullptr, false},
+                             const Bat& bt = Bat{}, int64_t zin = 0, int64_t zout = 0) {
     const int* flag = stop_eps > 0.f ? state : nullptr;
     int rc = 0;
     if (!chain.splatted) {
-        rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp);
+        rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp, Bat{bt.B, bt.slab, zin});
         if (rc) return rc;
     }
-    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next);
+    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next, bt);
     if (rc) return rc;
-    rc = launch_carry_scan_state(g, ws, flag, st);
+    rc = launch_carry_scan_state(g, ws, flag, st, bt);
     if (rc) return rc;
-    rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st, pairs);
+    rc = launch_write_field(d, g, ws, map, defect, targets, max_exc, flag, st, pairs, bt);
     if (rc) return rc;
     uint32_t* sn = chain.splat_next ? counts_next : nullptr;
     rc = pairs ? launch_sample_f32(pairs, g.k, pts_in, pts_out, n, 1, disp, flag, st, true, sn, chain.next_exc,
-                                   chain.next_disp, chain.sorted)
+                                   chain.next_disp, chain.sorted, bt, zin, zout)
                : launch_sample_f32(targets, g.k, pts_in, pts_out, n, 1, disp, flag, st, false, sn, chain.next_exc,
-                                   chain.next_disp, chain.sorted);
+                                   chain.next_disp, chain.sorted, bt, zin, zout);
     if (rc) return rc;
     if (flag) {
         INIM_CUDA_TRY(launch_pdl(iter_end_kernel, dim3(1), dim3(1), 0, st, (const float*)disp, stop_eps, state));
@@ -184,6 +188,7 @@ struct RunKey {
     const void *fstats, *orig_sub, *pick, *moved_sub, *nbstats;
     int64_t n_sub;
     int n_neighbors;
+    int B;  // plots in a batch (inim_run_batched), else 0
     bool operator==(const RunKey& o) const { return memcmp(this, &o, sizeof(RunKey)) == 0; }
 };
 
@@ -195,11 +200,18 @@ struct RunEntry {
 static std::mutex g_mu;
 static std::vector<RunEntry> g_cache;
 
+// The run (regularize.run's numeric loop) for one plot, or for a batch of key.B plots
+// with the plot index in every launch's grid.z (then frames / fields / disp /
+// excursions / state / neighbourhood metrics are not recorded: fixed iterations only).
 static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fields, float* disp, float* excursions,
                        int* state, void* ws, cudaStream_t st) {
     const Geo g = make_geo(key.k);
     const FullLayout F = full_layout(g, key.n);
     const Ws w = make_ws(ws, F.L);
+    const int B = key.B > 1 ? key.B : 1;
+    // plot strides: workspace slabs (bytes) and the caller's (B, n, 2) points (floats)
+    const Bat bt{B, B > 1 ? (int64_t)F.bytes : 0, B > 1 ? 2 * key.n : 0};
+    const int64_t zs = bt.slab / (int64_t)sizeof(float);  // slab stride in floats (workspace point buffers)
     char* base = static_cast<char*>(ws);
     uint32_t* counts = reinterpret_cast<uint32_t*>(base + F.counts);
     float* d = reinterpret_cast<float*>(base + F.d);
@@ -218,8 +230,11 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         mp = &map;
     }
     // once per run: the first count buffer cleared (iteration 0's smoothing clears the
-    // other one for iteration 1)
-    INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * g.m, st));
+    // other one for iteration 1); a batch clears every plot's with one 2-D memset
+    if (B > 1)
+        INIM_CUDA_TRY(cudaMemset2DAsync(counts, (size_t)bt.slab, 0, sizeof(uint32_t) * g.m, (size_t)B, st));
+    else
+        INIM_CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * g.m, st));
     prof_mark(st, "memset_counts");
     if (defect) {
         int rc = launch_flat_response(g.k, defect, st);
@@ -229,11 +244,12 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     if (frames && key.n > 0) INIM_CUDA_TRY(cudaMemcpyAsync(frames, pts, pbytes, cudaMemcpyDeviceToDevice, st));
     // Per-frame metrics: occupancy statistics of frame t+1 come off the counts the move
     // of iteration t splats (so the last move splats too); neighbourhood metrics of the
-    // fixed subsample against frame 0.
+    // fixed subsample against frame 0.  A batch keeps plot z's statistics at
+    // fstats[z][t][3].
     unsigned long long* fstats = (unsigned long long*)key.fstats;
     unsigned long long* nbstats = (unsigned long long*)key.nbstats;
-    const bool nb = fstats && key.orig_sub && nbstats && key.moved_sub && key.n_sub > 0;
-    if (fstats) INIM_CUDA_TRY(cudaMemsetAsync(fstats, 0, sizeof(unsigned long long) * 3 * key.iters, st));
+    const bool nb = fstats && key.orig_sub && nbstats && key.moved_sub && key.n_sub > 0 && B == 1;
+    if (fstats) INIM_CUDA_TRY(cudaMemsetAsync(fstats, 0, sizeof(unsigned long long) * 3 * key.iters * B, st));
     if (nb) INIM_CUDA_TRY(cudaMemsetAsync(nbstats, 0, sizeof(unsigned long long) * 2 * key.iters, st));
     // Spatial order: for runs long enough to amortise it, the points are sorted by pixel
     // once (from the counts of iteration 0's splat, which the run needs anyway), the
@@ -244,16 +260,17 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     auto exc_at = [&](int t) { return excursions ? excursions + t : scratch + 2 * (t & 1) + 1; };
     if (sorted) {
         const int* flag = key.eps > 0.f ? state : nullptr;
-        int rc = launch_splat_f32(pts, key.n, g.k, counts, flag, st, exc_at(0), disp_at(0));
+        int rc = launch_splat_f32(pts, key.n, g.k, counts, flag, st, exc_at(0), disp_at(0), bt);
         if (rc) return rc;
         // the other count buffer is the sort's cursor; iteration 0's smoothing clears it
         rc = launch_sort_points(pts, key.n, g.k, counts, counts + g.m, reinterpret_cast<uint32_t*>(hist), sortA,
-                                reinterpret_cast<uint32_t*>(perm), st);
+                                reinterpret_cast<uint32_t*>(perm), st, bt);
         if (rc) return rc;
     }
     // Point buffers: unsorted, the first move reads the caller's array and the last one
     // writes it back (no staging copies); in between the moves ping-pong through
-    // sortA / sortB.
+    // sortA / sortB.  Each buffer's plot stride: the caller's array bt.pts, the
+    // workspace buffers one slab.
     float* bufs[2] = {sortB, sortA};
     auto pos_in = [&](int t) -> float* {
         if (t == 0) return sorted ? sortA : pts;
@@ -263,6 +280,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         if (t == key.iters - 1 && !sorted) return pts;
         return bufs[(t + 1) & 1];
     };
+    auto zstride = [&](const float* p) -> int64_t { return p == pts ? bt.pts : zs; };
     // per-iteration device scalars: recorded arrays, else two alternating scratch slots
     // (the move of iteration t clears iteration t+1's slot while t's is still live)
     for (int t = 0; t < key.iters; ++t) {
@@ -280,7 +298,8 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         const bool pairs = use_pairs(g);
         float* plain = tg ? tg : (pairs ? nullptr : tg_scratch);
         int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, plain, exc_at(t),
-                                   disp_at(t), key.eps, state, w, mp, st, pairs ? tg_scratch : nullptr, chain);
+                                   disp_at(t), key.eps, state, w, mp, st, pairs ? tg_scratch : nullptr, chain, bt,
+                                   zstride(src), zstride(dst));
         if (rc) return rc;
         if (frames && key.n > 0) {
             float* fr = frames + (size_t)(t + 1) * 2 * key.n;
@@ -289,7 +308,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
             if (rc) return rc;
         }
         if (fstats && key.n > 0) {
-            rc = launch_frame_stats(next, g.k, fstats + 3 * t, st);
+            rc = launch_frame_stats(next, g.k, fstats + 3 * t, st, bt, 3 * (int64_t)key.iters);
             if (rc) return rc;
         }
         if (nb && key.n > 0) {
@@ -302,7 +321,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         }
     }
     if (sorted && key.iters > 0)
-        return launch_unpermute(pos_out(key.iters - 1), reinterpret_cast<const uint32_t*>(perm), key.n, pts, st);
+        return launch_unpermute(pos_out(key.iters - 1), reinterpret_cast<const uint32_t*>(perm), key.n, pts, st, bt);
     return 0;
 }
 
@@ -314,9 +333,9 @@ extern "C" {
 
 const char* inim_version(void) { return "libinim sm_100a 0.1"; }
 
-size_t inim_workspace_bytes(int k, int64_t n) {
-    if (!k_ok(k)) return 0;
-    return full_layout(make_geo(k), n).bytes;
+size_t inim_workspace_bytes(int k, int64_t n, int B) {
+    if (!k_ok(k) || n < 0) return 0;
+    return full_layout(make_geo(k), n).bytes * (size_t)(B > 1 ? B : 1);
 }
 
 int inim_splat(const void* pts, int pts_is_f64, int64_t n, int k, uint32_t* counts, cudaStream_t stream) {
@@ -536,6 +555,20 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
     return run_graph(key, pts, frames, fields, disp, excursions, state, ws, stream);
 }
 
+int inim_run_batched(float* pts, int64_t n, int B, int k, int kernel_size, float background, int iterations,
+                     unsigned long long* frame_stats, void* ws, cudaStream_t stream) {
+    if (k < 1 || k > INIM_MAX_K || n < 0 || B < 1 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
+    if (kernel_size < 1) return INIM_EKERNEL;
+    if (iterations == 0) return 0;
+    if (B > 1 && (n & 1)) return INIM_EINVAL;  // every plot's points 16-byte aligned (two points per access)
+    RunKey key;
+    memset(&key, 0, sizeof(key));
+    key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
+    key.iters = iterations; key.ws = ws; key.st = stream; key.B = B;
+    key.fstats = frame_stats;
+    return run_graph(key, pts, nullptr, nullptr, nullptr, nullptr, nullptr, ws, stream);
+}
+
 int inim_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t stream) {
     if (!k_ok(k) || !counts || !out3) return INIM_EINVAL;
     return launch_frame_stats(counts, k, out3, stream);
@@ -633,7 +666,7 @@ int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, in
     static cudaStream_t st = nullptr;
     std::lock_guard<std::mutex> lock(mu);
     if (!st) INIM_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    const size_t need = inim_workspace_bytes(k, n);
+    const size_t need = inim_workspace_bytes(k, n, 1);
     if (need > ws_bytes) {
         if (ws) cudaFree(ws);
         INIM_CUDA_TRY(cudaMalloc(&ws, need));

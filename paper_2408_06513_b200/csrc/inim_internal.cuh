@@ -10,6 +10,7 @@
 
 #include <mutex>
 #include <set>
+#include <type_traits>
 #include <utility>
 
 #include "inim_common.cuh"
@@ -166,6 +167,54 @@ inline Ws make_ws(void* base, const WsLayout& L) {
     return w;
 }
 
+// ---------------------------------------------------------------- plot batches
+// A batch of B independent plots (a SPLOM) runs every stage as ONE launch with the plot
+// index in blockIdx.z.  Each plot owns a slab of the workspace (inim_workspace_bytes(k,
+// n, 1) bytes, 256-aligned); plot z's workspace pointers are plot 0's plus z * slab
+// bytes, and its points are the caller's (B, n, 2) array at z * 2n floats.  B = 1 with
+// slab = 0 is the single-plot path (every offset is zero).
+struct Bat {
+    int B = 1;
+    int64_t slab = 0;  // bytes between consecutive plots' workspace slabs
+    int64_t pts = 0;   // floats between consecutive plots' caller point arrays
+};
+
+template <typename T>
+__host__ __device__ __forceinline__ T* zoff(T* p, int64_t bytes) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(const_cast<typename std::remove_const<T>::type*>(p)) + bytes);
+}
+template <typename T>
+__host__ __device__ __forceinline__ T* zoff_opt(T* p, int64_t bytes) {  // null stays null
+    return p ? zoff(p, bytes) : p;
+}
+
+__host__ __device__ __forceinline__ Ws ws_shift(Ws w, int64_t b) {
+    if (b == 0) return w;
+    w.tmp = zoff(w.tmp, b);
+    w.inpre = zoff(w.inpre, b);
+    w.tiletot = zoff(w.tiletot, b);
+    w.rowsum = zoff(w.rowsum, b);
+    w.ulbot = zoff(w.ulbot, b);
+    w.urbot = zoff(w.urbot, b);
+    w.ule = zoff(w.ule, b);
+    w.ure = zoff(w.ure, b);
+    w.tilepre = zoff(w.tilepre, b);
+    w.btot = zoff(w.btot, b);
+    w.bandpre = zoff(w.bandpre, b);
+    w.tlcar = zoff(w.tlcar, b);
+    w.x1 = zoff(w.x1, b);
+    w.x2 = zoff(w.x2, b);
+    w.hc = zoff(w.hc, b);
+    w.rpre = zoff(w.rpre, b);
+    w.taps = zoff(w.taps, b);
+    w.total = zoff(w.total, b);
+    w.misc = zoff(w.misc, b);
+    return w;
+}
+
+// byte offset of this CTA's plot
+INIM_DEV int64_t zslab_off(int64_t slab) { return (int64_t)blockIdx.z * slab; }
+
 // ---------------------------------------------------------------- launch profiler
 // When g_prof is set (inim_profile_run only), every launcher records a CUDA event
 // after its launch; consecutive events bracket exactly one launch.
@@ -185,14 +234,15 @@ inline void prof_mark(cudaStream_t st, const char* name) {
 
 // ---------------------------------------------------------------- host-side launchers
 int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map,
-                              cudaStream_t st);
-int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st);
+                              cudaStream_t st, const Bat& bt = Bat{});
+int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st, const Bat& bt = Bat{});
 int launch_write_tables(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, float* tables8,
                         cudaStream_t st);
 // targets: standard (s, s, 2) field or null; pairs: paired (s, s, 4) layout for the
 // move kernel or null.
 int launch_write_field(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const float* defect,
-                       float* targets, float* max_exc, const int* state, cudaStream_t st, float* pairs = nullptr);
+                       float* targets, float* max_exc, const int* state, cudaStream_t st, float* pairs = nullptr,
+                       const Bat& bt = Bat{});
 int make_tensor_map_2d(CUtensorMap* map, const float* base, int s, int box_w, int box_h);
 
 }  // namespace inim

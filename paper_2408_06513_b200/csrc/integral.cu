@@ -33,7 +33,7 @@ __host__ __device__ inline size_t ring_smem_bytes(const Geo& g) {
 template <int CPL>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_ring_kernel(const __grid_constant__ CUtensorMap map,
                                                                         const Geo g, const Ws ws) {
-    pdl_enter();
+    pdl_enter();  // (standalone API only: one plot)
     extern __shared__ __align__(128) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles = g.B * g.NX;
@@ -115,8 +115,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_ring_kernel(const __
 // registers), so residency is bounded by registers only.
 template <int CPL>
 __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* __restrict__ d, const Geo g,
-                                                                   const Ws ws) {
+                                                                   const Ws ws0, int64_t zslab) {
     pdl_enter();
+    const int64_t zo = zslab_off(zslab);
+    d = zoff(d, zo);
+    const Ws ws = ws_shift(ws0, zo);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kWarpsPerCta + w;
     if (tile >= g.B * g.NX) return;
@@ -128,9 +131,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* 
 // ahead in registers): no shared memory, so residency is bounded by registers only.
 template <int CPL, int MODE>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, CPL == 4 ? 5 : 1) write_kernel(const float* __restrict__ d, const Geo g,
-                                                                  const Ws ws, const WriteOut out, const int* state) {
+                                                                  const Ws ws0, const WriteOut out0, const int* state,
+                                                                  int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;  // displacement stop already reached
+    const int64_t zo = zslab_off(zslab);  // plot blockIdx.z of a batch
+    d = zoff(d, zo);
+    const Ws ws = ws_shift(ws0, zo);
+    WriteOut out = out0;
+    if (zo) {
+        out.targets = zoff_opt(out.targets, zo);
+        out.max_exc = zoff_opt(out.max_exc, zo);
+        out.pairs = zoff_opt(out.pairs, zo);
+    }
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kWarpsPerCta + w;
     if (tile >= g.B * g.NX) return;
@@ -233,8 +246,8 @@ static unsigned tile_ctas(const Geo& g) { return (unsigned)((g.B * g.NX + kWarps
 
 template <int CPL>
 static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* ring_map,
-                             cudaStream_t st) {
-    if (ring_map && g.TH % kChunk == 0 && g.TW >= 32) {
+                             cudaStream_t st, const Bat& bt) {
+    if (ring_map && g.TH % kChunk == 0 && g.TW >= 32 && bt.B == 1) {
         const size_t smem = ring_smem_bytes(g);
         INIM_CUDA_TRY(ensure_smem_limit((const void*)reduce_ring_kernel<CPL>, (int)smem));
         // one tile per warp: persistent warps (grid capped at residency, several tiles
@@ -243,36 +256,38 @@ static int launch_reduce_cpl(const float* d, const Geo& g, const Ws& ws, const C
         INIM_CUDA_TRY(launch_pdl(reduce_ring_kernel<CPL>, dim3(ctas), dim3(kWarpsPerCta * 32), smem, st, *ring_map, g,
                                  ws));
     } else {
-        INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws));
+        INIM_CUDA_TRY(launch_pdl(reduce_kernel<CPL>, dim3(tile_ctas(g), 1, bt.B), dim3(kWarpsPerCta * 32), 0, st, d, g,
+                                 ws, bt.slab));
     }
     prof_mark(st, "reduce");
     return (int)cudaGetLastError();
 }
 
-int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, cudaStream_t st) {
+int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, cudaStream_t st,
+                              const Bat& bt) {
     switch (g.CPL) {
-        case 4: return launch_reduce_cpl<4>(d, g, ws, map, st);
-        case 2: return launch_reduce_cpl<2>(d, g, ws, map, st);
-        default: return launch_reduce_cpl<1>(d, g, ws, map, st);
+        case 4: return launch_reduce_cpl<4>(d, g, ws, map, st, bt);
+        case 2: return launch_reduce_cpl<2>(d, g, ws, map, st, bt);
+        default: return launch_reduce_cpl<1>(d, g, ws, map, st, bt);
     }
 }
 
 template <int CPL, int MODE>
 static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const WriteOut& out, const int* state,
-                            cudaStream_t st) {
-    INIM_CUDA_TRY(launch_pdl(write_kernel<CPL, MODE>, dim3(tile_ctas(g)), dim3(kWarpsPerCta * 32), 0, st, d, g, ws,
-                             out, state));
+                            cudaStream_t st, const Bat& bt) {
+    INIM_CUDA_TRY(launch_pdl(write_kernel<CPL, MODE>, dim3(tile_ctas(g), 1, bt.B), dim3(kWarpsPerCta * 32), 0, st, d,
+                             g, ws, out, state, bt.slab));
     prof_mark(st, MODE == 0 ? "write_tables" : "write_field");
     return (int)cudaGetLastError();
 }
 
 template <int MODE>
 static int launch_write_mode(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const WriteOut& out,
-                             const int* state, cudaStream_t st) {
+                             const int* state, cudaStream_t st, const Bat& bt = Bat{}) {
     switch (g.CPL) {
-        case 4: return launch_write_cpl<4, MODE>(d, g, ws, out, state, st);
-        case 2: return launch_write_cpl<2, MODE>(d, g, ws, out, state, st);
-        default: return launch_write_cpl<1, MODE>(d, g, ws, out, state, st);
+        case 4: return launch_write_cpl<4, MODE>(d, g, ws, out, state, st, bt);
+        case 2: return launch_write_cpl<2, MODE>(d, g, ws, out, state, st, bt);
+        default: return launch_write_cpl<1, MODE>(d, g, ws, out, state, st, bt);
     }
 }
 
@@ -283,9 +298,10 @@ int launch_write_tables(const float* d, const Geo& g, const Ws& ws, const CUtens
 }
 
 int launch_write_field(const float* d, const Geo& g, const Ws& ws, const CUtensorMap* map, const float* defect,
-                       float* targets, float* max_exc, const int* state, cudaStream_t st, float* pairs) {
+                       float* targets, float* max_exc, const int* state, cudaStream_t st, float* pairs, const Bat& bt) {
     WriteOut o{nullptr, targets, defect, max_exc, pairs};
-    return defect ? launch_write_mode<2>(d, g, ws, map, o, state, st) : launch_write_mode<1>(d, g, ws, map, o, state, st);
+    return defect ? launch_write_mode<2>(d, g, ws, map, o, state, st, bt)
+                  : launch_write_mode<1>(d, g, ws, map, o, state, st, bt);
 }
 
 int launch_field_from_tables(const float* t8, int k, const double* total, const float* defect, float* targets,

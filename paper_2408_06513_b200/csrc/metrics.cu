@@ -32,8 +32,11 @@ INIM_DEV T block_sum(T v, T* red) {
 // nonzero counts.  out[0] += occupied pixels, out[1] += sum over bins of count^2,
 // out[2] += sum of counts (= n).  One thread per bin; each of its four rows is one
 // 16-byte load, consecutive threads read consecutive bins of a row (coalesced).
-__global__ void __launch_bounds__(256) frame_stats_kernel(const uint32_t* __restrict__ counts, int k, u64* out) {
+__global__ void __launch_bounds__(256) frame_stats_kernel(const uint32_t* __restrict__ counts, int k, u64* out,
+                                                          int64_t zslab, int64_t zout) {
     pdl_enter();
+    counts = zoff(counts, zslab_off(zslab));  // plot blockIdx.z of a batch
+    out += blockIdx.z * zout;
     __shared__ u64 red[8];
     const int s = 1 << k;
     u64 occ = 0, sq = 0, tot = 0;
@@ -224,9 +227,11 @@ static unsigned blocks_for(int64_t work, int per_block, int per_sm) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
-int launch_frame_stats(const uint32_t* counts, int k, u64* out3, cudaStream_t st) {
+// zout: u64 between consecutive plots' outputs of a batch
+int launch_frame_stats(const uint32_t* counts, int k, u64* out3, cudaStream_t st, const Bat& bt, int64_t zout) {
     const int64_t bins = k >= 2 ? ((int64_t)1 << (2 * k - 4)) : 1;
-    INIM_CUDA_TRY(launch_pdl(frame_stats_kernel, dim3(blocks_for(bins, 256, 8)), dim3(256), 0, st, counts, k, out3));
+    INIM_CUDA_TRY(launch_pdl(frame_stats_kernel, dim3(blocks_for(bins, 256, bt.B > 1 ? 1 : 8), 1, bt.B), dim3(256), 0,
+                             st, counts, k, out3, bt.slab, zout));
     prof_mark(st, "frame_stats");
     return (int)cudaGetLastError();
 }

@@ -21,11 +21,19 @@ __device__ __forceinline__ void splat_one(uint32_t* counts, int pix) {
 // share a pixel: plain red.global.add (no return) per point, two points per 16-byte
 // load.  zero0/zero1: per-iteration device scalars (max excursion, max displacement)
 // cleared here so the iteration needs no separate reset launch.
-__global__ void __launch_bounds__(256) splat_f32_kernel(const float4* __restrict__ pts2, const float* __restrict__ pts,
-                                                        int64_t n, int k, uint32_t* __restrict__ counts,
-                                                        const int* state, float* zero0, float* zero1) {
+__global__ void __launch_bounds__(256) splat_f32_kernel(const float* __restrict__ pts, int64_t n, int k,
+                                                        uint32_t* __restrict__ counts, const int* state, float* zero0,
+                                                        float* zero1, int64_t zpts, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    {  // plot blockIdx.z of a batch
+        const int64_t zo = zslab_off(zslab);
+        pts += blockIdx.z * zpts;
+        counts = zoff(counts, zo);
+        zero0 = zoff_opt(zero0, zo);
+        zero1 = zoff_opt(zero1, zo);
+    }
+    const float4* __restrict__ pts2 = reinterpret_cast<const float4*>(pts);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (zero0) *zero0 = 0.f;
         if (zero1) *zero1 = 0.f;
@@ -77,13 +85,24 @@ __device__ __forceinline__ void move_point(const float* tg, int s, float x, floa
 }
 
 template <bool PAIRS, int U>
-__global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict__ tg, int k,
-                                                         const float4* __restrict__ in2, const float* __restrict__ in,
-                                                         float4* __restrict__ out2, float* __restrict__ out, int64_t n,
-                                                         int clip, float* max_disp, const int* state,
+__global__ void __launch_bounds__(256, 5) sample_f32_kernel(const float* __restrict__ tg, int k,
+                                                         const float* __restrict__ in, float* __restrict__ out,
+                                                         int64_t n, int clip, float* max_disp, const int* state,
                                                          uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
-                                                         int agg) {
+                                                         int agg, int64_t zin, int64_t zout, int64_t zslab) {
     pdl_enter();
+    {  // plot blockIdx.z of a batch
+        const int64_t zo = zslab_off(zslab);
+        tg = zoff(tg, zo);
+        in += blockIdx.z * zin;
+        out += blockIdx.z * zout;
+        max_disp = zoff_opt(max_disp, zo);
+        splat_next = zoff_opt(splat_next, zo);
+        zn0 = zoff_opt(zn0, zo);
+        zn1 = zoff_opt(zn1, zo);
+    }
+    const float4* __restrict__ in2 = reinterpret_cast<const float4*>(in);
+    float4* __restrict__ out2 = reinterpret_cast<float4*>(out);
     const bool stopped = state && state[0];
     const int s = 1 << k;
     // fused splat of the next iteration (its count buffer was cleared by this
@@ -195,8 +214,10 @@ constexpr int kScanItems = 16;                     // counts per thread
 constexpr int kScanBlock = 256 * kScanItems;       // counts per block
 
 __global__ void __launch_bounds__(256) scan_block_sums_kernel(const uint32_t* __restrict__ counts, int64_t m,
-                                                              uint32_t* __restrict__ bsum) {
+                                                              uint32_t* __restrict__ bsum, int64_t zslab) {
     pdl_enter();
+    counts = zoff(counts, zslab_off(zslab));
+    bsum = zoff(bsum, zslab_off(zslab));
     const int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
     uint32_t v = 0;
 #pragma unroll
@@ -218,8 +239,9 @@ __global__ void __launch_bounds__(256) scan_block_sums_kernel(const uint32_t* __
 }
 
 // one CTA: exclusive scan of the block sums in place
-__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ bsum, int nb) {
+__global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ bsum, int nb, int64_t zslab) {
     pdl_enter();
+    bsum = zoff(bsum, zslab_off(zslab));
     __shared__ uint32_t ws[33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t carry = 0;
@@ -252,8 +274,11 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ b
 
 __global__ void __launch_bounds__(256) scan_blocks_kernel(const uint32_t* __restrict__ counts, int64_t m,
                                                           const uint32_t* __restrict__ bsum,
-                                                          uint32_t* __restrict__ offsets) {
+                                                          uint32_t* __restrict__ offsets, int64_t zslab) {
     pdl_enter();
+    counts = zoff(counts, zslab_off(zslab));
+    bsum = zoff(bsum, zslab_off(zslab));
+    offsets = zoff(offsets, zslab_off(zslab));
     const int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
     uint32_t c[kScanItems];
     uint32_t v = 0;
@@ -288,8 +313,15 @@ __global__ void __launch_bounds__(256) scan_blocks_kernel(const uint32_t* __rest
 
 __global__ void __launch_bounds__(256) place_points_kernel(const float2* __restrict__ pts, int64_t n, int k,
                                                            uint32_t* __restrict__ cursor, float2* __restrict__ sorted,
-                                                           uint32_t* __restrict__ rank) {
+                                                           uint32_t* __restrict__ rank, int64_t zpts, int64_t zslab) {
     pdl_enter();
+    {
+        const int64_t zo = zslab_off(zslab);
+        pts += blockIdx.z * (zpts >> 1);
+        cursor = zoff(cursor, zo);
+        sorted = zoff(sorted, zo);
+        rank = zoff(rank, zo);
+    }
     const int s = 1 << k;
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -319,8 +351,11 @@ __global__ void __launch_bounds__(256) place_points_kernel(const float2* __restr
 // out[p] = sorted[rank[p]]: coalesced rank reads and output writes, gathered reads.
 __global__ void __launch_bounds__(256) unpermute_kernel(const float2* __restrict__ sorted,
                                                         const uint32_t* __restrict__ rank, int64_t n,
-                                                        float2* __restrict__ out) {
+                                                        float2* __restrict__ out, int64_t zout, int64_t zslab) {
     pdl_enter();
+    sorted = zoff(sorted, zslab_off(zslab));
+    rank = zoff(rank, zslab_off(zslab));
+    out += blockIdx.z * (zout >> 1);
     constexpr int U = 4;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += U * stride) {
@@ -389,11 +424,20 @@ static unsigned grid_for(int64_t work, int per_block) {
     return (unsigned)(blocks < 1 ? 1 : blocks);
 }
 
+// Batches: one launch covers every plot (grid.z = plot); the per-plot grid is not
+// capped at one resident wave, B of them fill the GPU.
+static dim3 batch_grid(unsigned per_plot_resident, int64_t work, int per_block, const Bat& bt) {
+    if (bt.B <= 1) return dim3(per_plot_resident);
+    int64_t blocks = (work + per_block - 1) / per_block;
+    return dim3((unsigned)(blocks < 1 ? 1 : blocks), 1, (unsigned)bt.B);
+}
+
 int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const int* state, cudaStream_t st,
-                     float* zero0, float* zero1) {
+                     float* zero0, float* zero1, const Bat& bt) {
     const int64_t npair = n >> 1;
-    INIM_CUDA_TRY(launch_pdl(splat_f32_kernel, dim3(grid_for(npair > 0 ? npair : 1, 256)), dim3(256), 0, st,
-                             reinterpret_cast<const float4*>(pts), pts, n, k, counts, state, zero0, zero1));
+    const dim3 grid = batch_grid(grid_for(npair > 0 ? npair : 1, 256), npair, 256 * 4, bt);
+    INIM_CUDA_TRY(launch_pdl(splat_f32_kernel, grid, dim3(256), 0, st, pts, n, k, counts, state, zero0, zero1, bt.pts,
+                             bt.slab));
     prof_mark(st, "splat");
     return (int)cudaGetLastError();
 }
@@ -401,16 +445,17 @@ int launch_splat_f32(const float* pts, int64_t n, int k, uint32_t* counts, const
 // Sort the points by pixel: `counts` are the points' per-pixel counts (the run's first
 // splat), `cursor` an m-word scratch (destroyed), bsum ceil(m / kScanBlock) words.
 int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* counts, uint32_t* cursor,
-                       uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st) {
+                       uint32_t* bsum, float* sorted, uint32_t* rank, cudaStream_t st, const Bat& bt) {
     const int64_t m = (int64_t)1 << (2 * k);
     const unsigned nb = (unsigned)((m + kScanBlock - 1) / kScanBlock);
-    INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb), dim3(256), 0, st, counts, m, bsum));
-    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb));
-    INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb), dim3(256), 0, st, counts, m, (const uint32_t*)bsum,
-                             cursor));
-    INIM_CUDA_TRY(launch_pdl(place_points_kernel, dim3(grid_for(n > 0 ? n : 1, 256)), dim3(256), 0, st,
-                             reinterpret_cast<const float2*>(pts), n, k, cursor, reinterpret_cast<float2*>(sorted),
-                             rank));
+    const unsigned z = (unsigned)bt.B;
+    INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb, 1, z), dim3(256), 0, st, counts, m, bsum, bt.slab));
+    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1, 1, z), dim3(1024), 0, st, bsum, (int)nb, bt.slab));
+    INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb, 1, z), dim3(256), 0, st, counts, m, (const uint32_t*)bsum,
+                             cursor, bt.slab));
+    INIM_CUDA_TRY(launch_pdl(place_points_kernel, batch_grid(grid_for(n > 0 ? n : 1, 256), n, 256, bt), dim3(256), 0,
+                             st, reinterpret_cast<const float2*>(pts), n, k, cursor, reinterpret_cast<float2*>(sorted),
+                             rank, bt.pts, bt.slab));
     prof_mark(st, "sort_points");
     return (int)cudaGetLastError();
 }
@@ -418,17 +463,20 @@ int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* count
 // Exclusive prefix of m (a multiple of 4) u32 counts into `out`; bsum: sort_bsum_words.
 int launch_exclusive_scan_u32(const uint32_t* counts, int64_t m, uint32_t* bsum, uint32_t* out, cudaStream_t st) {
     const unsigned nb = (unsigned)((m + kScanBlock - 1) / kScanBlock);
-    INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb), dim3(256), 0, st, counts, m, bsum));
-    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb));
-    INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb), dim3(256), 0, st, counts, m, (const uint32_t*)bsum, out));
+    INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb), dim3(256), 0, st, counts, m, bsum, (int64_t)0));
+    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb, (int64_t)0));
+    INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb), dim3(256), 0, st, counts, m, (const uint32_t*)bsum, out,
+                             (int64_t)0));
     return (int)cudaGetLastError();
 }
 
 size_t sort_bsum_words(int k) { return (size_t)((((int64_t)1 << (2 * k)) + kScanBlock - 1) / kScanBlock); }
 
-int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st) {
-    INIM_CUDA_TRY(launch_pdl(unpermute_kernel, dim3(grid_for(n > 0 ? n : 1, 256)), dim3(256), 0, st,
-                             reinterpret_cast<const float2*>(sorted), rank, n, reinterpret_cast<float2*>(out)));
+int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st,
+                     const Bat& bt) {
+    INIM_CUDA_TRY(launch_pdl(unpermute_kernel, batch_grid(grid_for(n > 0 ? n : 1, 256), n, 256 * 4, bt), dim3(256), 0,
+                             st, reinterpret_cast<const float2*>(sorted), rank, n, reinterpret_cast<float2*>(out),
+                             bt.pts, bt.slab));
     prof_mark(st, "unpermute");
     return (int)cudaGetLastError();
 }
@@ -438,16 +486,18 @@ int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cuda
     return (int)cudaGetLastError();
 }
 
+// zin / zout: floats between consecutive plots' input / output points (a batch reads
+// the caller's (B, n, 2) array or the workspace ping-pong buffers).
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
                       const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1,
-                      bool sorted) {
+                      bool sorted, const Bat& bt, int64_t zin, int64_t zout) {
     const int64_t npair = n >> 1;
     // two point pairs (two 16-byte loads) per thread per step (measured: 1 or 4 are
     // slower at C2)
     auto kern = pairs ? sample_f32_kernel<true, 2> : sample_f32_kernel<false, 2>;
-    INIM_CUDA_TRY(launch_pdl(kern, dim3(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256)), dim3(256), 0,
-                             st, tg, k, reinterpret_cast<const float4*>(in), in, reinterpret_cast<float4*>(out), out, n,
-                             clip, max_disp, state, splat_next, zn0, zn1, sorted ? 1 : 0));
+    const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair, 256 * 2, bt);
+    INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, in, out, n, clip, max_disp, state, splat_next, zn0,
+                             zn1, sorted ? 1 : 0, zin, zout, bt.slab));
     prof_mark(st, "sample");
     return (int)cudaGetLastError();
 }

@@ -7,18 +7,16 @@
 
 namespace inim {
 
-// INIM_CHAIN_MINB: experiment switch (measured: forcing 4 CTAs/SM = 32 registers spills
-// and is no faster than 3 CTAs/SM).  Left undefined on purpose: an explicit minimum of 1
-// lets ptxas spend 72 registers (1 CTA/SM, -4% on the integral sweep), while the plain
-// bound settles at 40 (3 CTAs/SM).
-#ifdef INIM_CHAIN_MINB
-#define INIM_CHAIN_BOUNDS __launch_bounds__(512, INIM_CHAIN_MINB)
-#else
-#define INIM_CHAIN_BOUNDS __launch_bounds__(512)
-#endif
-__global__ void INIM_CHAIN_BOUNDS chains_kernel(const Geo g, const Ws ws, const int* state) {
+// Launch bounds: the plain 512-thread bound settles at 40 registers (3 CTAs/SM),
+// measured best (an explicit minimum of 1 CTA/SM lets ptxas spend 72
+// registers and costs 4% of the 16384^2 integral pass; 4 CTAs/SM spill).  BATCH: the
+// plot offsets of a SPLOM batch (grid.z) are a separate instantiation, so the
+// single-plot kernels keep their register budget.
+template <bool BATCH>
+__global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    const Ws ws = BATCH ? ws_shift(ws0, zslab_off(zslab)) : ws0;
     __shared__ double part[16][33];
     __shared__ double bp[kMaxBands + 1];
     __shared__ double sh[33];
@@ -34,10 +32,11 @@ __global__ void INIM_CHAIN_BOUNDS chains_kernel(const Geo g, const Ws ws, const 
 }
 
 // Single-read chains: each thread holds its chunk of step terms in registers.
-template <int MAXCH>
-__global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws ws, const int* state) {
+template <int MAXCH, bool BATCH>
+__global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    const Ws ws = BATCH ? ws_shift(ws0, zslab_off(zslab)) : ws0;
     __shared__ double part[16][33];
     __shared__ double bp[kMaxBands + 1];
     __shared__ double sh[33];
@@ -48,9 +47,10 @@ __global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws w
 // tiles of row j's tile row sums, rpre = the band's in-band prefix of the row totals,
 // tilepre / btot = the exclusive prefix and the total of the band's tile totals.  A
 // launch of its own so that no reduce warp has to fence and count its band's arrivals.
-__global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws, const int* state) {
+__global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    const Ws ws = ws_shift(ws0, zslab_off(zslab));
     __shared__ double rowtot[32];
     const int b = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TH = g.TH, NX = g.NX, a = b * TH;
@@ -70,18 +70,21 @@ __global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws, c
     }
 }
 
-int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st) {
-    INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B), dim3(32 * g.TH), 0, st, g, ws, state));
+int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st, const Bat& bt) {
+    INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B, 1, bt.B), dim3(32 * g.TH), 0, st, g, ws, state, bt.slab));
     prof_mark(st, "lines");
     const int ny = chain_warps(g), ch = (g.B + ny - 1) / ny;
-    const dim3 grid(chains_items(g)), block(32 * ny);
+    const dim3 grid(chains_items(g), 1, bt.B), block(32 * ny);
     // register-held chunks pay off only while they are short (measured: 1024^2 +7% on
     // the integral sweep; 4096^2 +-0; 8192^2 and up -10%, occupancy); longer chunks run
     // the two-pass kernel
+    const bool batch = bt.B > 1;
     if (ch <= 4) {
-        INIM_CUDA_TRY(launch_pdl(chains_reg_kernel<4>, grid, block, 0, st, g, ws, state));
+        INIM_CUDA_TRY(launch_pdl(batch ? chains_reg_kernel<4, true> : chains_reg_kernel<4, false>, grid, block, 0, st,
+                                 g, ws, state, bt.slab));
     } else {
-        INIM_CUDA_TRY(launch_pdl(chains_kernel, grid, block, 0, st, g, ws, state));
+        INIM_CUDA_TRY(launch_pdl(batch ? chains_kernel<true> : chains_kernel<false>, grid, block, 0, st, g, ws, state,
+                                 bt.slab));
     }
     prof_mark(st, "chains");
     return (int)cudaGetLastError();

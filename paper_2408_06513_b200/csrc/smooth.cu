@@ -13,9 +13,15 @@ namespace inim {
 template <int R, typename T>
 __global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
-                                                       uint32_t* __restrict__ zero_next) {
+                                                       uint32_t* __restrict__ zero_next, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    if (zslab) {  // plot blockIdx.z of a batch (the input is the plot's counts)
+        const int64_t zo = zslab_off(zslab);
+        in = zoff(in, zo);
+        out = zoff(out, zo);
+        zero_next = zoff_opt(zero_next, zo);
+    }
     extern __shared__ __align__(16) float hsm[];
     smooth_h_tile<R, T>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
 }
@@ -23,11 +29,13 @@ __global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) sm
 template <int R>
 __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__ tmp, float* __restrict__ d,
                                                        const Geo g, const VGeo v, const Ws ws, const Taps taps,
-                                                       float background, int emit, const int* state) {
+                                                       float background, int emit, const int* state, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
-    smooth_v_tile<R>(tmp, d, g, v, ws, taps, background, emit, blockIdx.x, blockIdx.y, vsm);
+    const int64_t zo = zslab_off(zslab);
+    smooth_v_tile<R>(zoff(tmp, zo), zoff(d, zo), g, v, ws_shift(ws, zo), taps, background, emit, blockIdx.x,
+                     blockIdx.y, vsm);
 }
 
 // ------------------------------------------------------- generic taps (kernel_size > 16)
@@ -44,8 +52,9 @@ struct GenericTaps {
     double sigma, inv_tot;
 };
 
-__global__ void generic_taps_kernel(float* __restrict__ taps, int s, const GenericTaps gt) {
+__global__ void generic_taps_kernel(float* __restrict__ taps, int s, const GenericTaps gt, int64_t zslab) {
     pdl_enter();
+    taps = zoff(taps, zslab_off(zslab));
     const int64_t period = 2 * (int64_t)s;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < gt.nt; q += gridDim.x * blockDim.x) {
         double acc = 0.0;
@@ -67,9 +76,17 @@ __global__ void generic_taps_kernel(float* __restrict__ taps, int s, const Gener
 template <typename T>
 __global__ void __launch_bounds__(256) generic_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                         const float* __restrict__ taps, const GenericTaps gt,
-                                                        const int* state, uint32_t* __restrict__ zero_next) {
+                                                        const int* state, uint32_t* __restrict__ zero_next,
+                                                        int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    {
+        const int64_t zo = zslab_off(zslab);
+        in = zoff(in, zo);
+        out = zoff(out, zo);
+        taps = zoff(taps, zo);
+        zero_next = zoff_opt(zero_next, zo);
+    }
     const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
     if (i >= s) return;
     const T* row = in + (int64_t)j * s;
@@ -81,9 +98,15 @@ __global__ void __launch_bounds__(256) generic_h_kernel(const T* __restrict__ in
 
 __global__ void __launch_bounds__(256) generic_v_kernel(const float* __restrict__ tmp, float* __restrict__ d, int s,
                                                         const float* __restrict__ taps, const GenericTaps gt,
-                                                        float background, const int* state) {
+                                                        float background, const int* state, int64_t zslab) {
     pdl_enter();
     if (state && state[0]) return;
+    {
+        const int64_t zo = zslab_off(zslab);
+        tmp = zoff(tmp, zo);
+        d = zoff(d, zo);
+        taps = zoff(taps, zo);
+    }
     const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
     if (i >= s) return;
     float acc = 0.f;
@@ -93,7 +116,8 @@ __global__ void __launch_bounds__(256) generic_v_kernel(const float* __restrict_
 }
 
 static int launch_generic(const void* in, bool counts, const Geo& g, const Ws& ws, int kernel_size, float bg,
-                          float* d, bool emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
+                          float* d, bool emit, const int* state, uint32_t* zero_next, cudaStream_t st,
+                          const Bat& bt) {
     GenericTaps gt;
     const int64_t R64 = 3 * (int64_t)kernel_size;
     if (R64 > (int64_t)1 << 29) return INIM_EKERNEL;  // 6*ks+1 taps beyond int range
@@ -110,19 +134,21 @@ static int launch_generic(const void* in, bool counts, const Geo& g, const Ws& w
     const bool fold = 2 * (int64_t)gt.R + 1 > 2 * (int64_t)g.s;
     gt.nt = fold ? 2 * g.s : 2 * gt.R + 1;
     gt.o0 = fold ? 0 : -gt.R;
-    INIM_CUDA_TRY(launch_pdl(generic_taps_kernel, dim3((gt.nt + 255) / 256), dim3(256), 0, st, ws.taps, g.s, gt));
-    const dim3 grid((g.s + 255) / 256, g.s), block(256);
+    const unsigned z = (unsigned)bt.B;
+    INIM_CUDA_TRY(launch_pdl(generic_taps_kernel, dim3((gt.nt + 255) / 256, 1, z), dim3(256), 0, st, ws.taps, g.s, gt,
+                             bt.slab));
+    const dim3 grid((g.s + 255) / 256, g.s, z), block(256);
     if (counts)
         INIM_CUDA_TRY(launch_pdl(generic_h_kernel<uint32_t>, grid, block, 0, st, static_cast<const uint32_t*>(in),
-                                 ws.tmp, g.s, (const float*)ws.taps, gt, state, zero_next));
+                                 ws.tmp, g.s, (const float*)ws.taps, gt, state, zero_next, bt.slab));
     else
         INIM_CUDA_TRY(launch_pdl(generic_h_kernel<float>, grid, block, 0, st, static_cast<const float*>(in), ws.tmp,
-                                 g.s, (const float*)ws.taps, gt, state, zero_next));
+                                 g.s, (const float*)ws.taps, gt, state, zero_next, bt.slab));
     prof_mark(st, "smooth_h");
     INIM_CUDA_TRY(launch_pdl(generic_v_kernel, grid, block, 0, st, (const float*)ws.tmp, d, g.s,
-                             (const float*)ws.taps, gt, bg, state));
+                             (const float*)ws.taps, gt, bg, state, bt.slab));
     prof_mark(st, "smooth_v");
-    if (emit) return launch_reduce_from_global(d, g, ws, nullptr, st);  // the integral pass's tile aggregates
+    if (emit) return launch_reduce_from_global(d, g, ws, nullptr, st, bt);  // the integral pass's tile aggregates
     return (int)cudaGetLastError();
 }
 
@@ -143,54 +169,55 @@ void make_taps(int kernel_size, Taps* taps) {
 
 template <int R, typename T>
 static int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, uint32_t* zero_next,
-                    cudaStream_t st) {
+                    cudaStream_t st, const Bat& bt) {
     const HGeo h = make_hgeo(s);
     const size_t smem = h_smem_bytes(h, R);
     INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_h_kernel<R, T>, 200 * 1024));
-    dim3 grid(s / h.TWH, s / h.RH);
+    dim3 grid(s / h.TWH, s / h.RH, bt.B);
     INIM_CUDA_TRY(launch_pdl(smooth_h_kernel<R, T>, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state,
-                             zero_next));
+                             zero_next, bt.slab));
     prof_mark(st, "smooth_h");
     return (int)cudaGetLastError();
 }
 
 template <int R>
 static int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, const Taps& taps, float bg, int emit,
-                    const int* state, cudaStream_t st) {
+                    const int* state, cudaStream_t st, const Bat& bt) {
 
     const VGeo v = make_vgeo(g);
     const size_t smem = v_smem_bytes(g, v, R);
     INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_v_kernel<R>, 227 * 1024));
-    dim3 grid(g.NX, g.s / v.VR);
+    dim3 grid(g.NX, g.s / v.VR, bt.B);
     INIM_CUDA_TRY(launch_pdl(smooth_v_kernel<R>, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
-                             state));
+                             state, bt.slab));
     prof_mark(st, emit ? "smooth_v_reduce" : "smooth_v");
     return (int)cudaGetLastError();
 }
 
 template <int KS>
 static int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
-                       float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st) {
+                       float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt) {
     constexpr int R = 3 * KS;
-    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st)
-                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st);
+    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st,
+                                            bt)
+                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st, bt);
     if (rc) return rc;
-    return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st);
+    return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st, bt);
 }
 
 int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
                         float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
-                        uint32_t* zero_next) {
+                        uint32_t* zero_next, const Bat& bt) {
     if (kernel_size < 1) return INIM_EKERNEL;
     if (3 * kernel_size > kMaxR)
         return launch_generic(in, in_is_counts, g, ws, kernel_size, background, d, emit_aggregates, state, zero_next,
-                              st);
+                              st, bt);
     Taps taps;
     make_taps(kernel_size, &taps);
     const int emit = emit_aggregates ? 1 : 0;
     switch (kernel_size) {
 #define INIM_KS(K) \
-    case K: return launch_pair<K>(in, in_is_counts, g, ws, taps, background, d, emit, state, zero_next, st);
+    case K: return launch_pair<K>(in, in_is_counts, g, ws, taps, background, d, emit, state, zero_next, st, bt);
         INIM_KS(1) INIM_KS(2) INIM_KS(3) INIM_KS(4) INIM_KS(5) INIM_KS(6) INIM_KS(7) INIM_KS(8)
         INIM_KS(9) INIM_KS(10) INIM_KS(11) INIM_KS(12) INIM_KS(13) INIM_KS(14) INIM_KS(15) INIM_KS(16)
 #undef INIM_KS

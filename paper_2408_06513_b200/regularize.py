@@ -86,7 +86,7 @@ def _run_buffers(n: int, k: int, chunk: int, store_fields: bool):
         s = 1 << k
         dev = D.device()
         b = {
-            "ws": torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev),
+            "ws": torch.empty(int(lib.inim_workspace_bytes(k, n, 1)), dtype=torch.uint8, device=dev),
             "pts": torch.empty((max(n, 1), 2), dtype=torch.float32, device=dev),
             "frames": torch.empty((chunk + 1, max(n, 1), 2), dtype=torch.float32, device=dev),
             "fields": torch.empty((chunk, s, s, 2), dtype=torch.float32, device=dev) if store_fields else None,

@@ -3,14 +3,15 @@
 
 Plots are independent (no cross-plot term anywhere in the reference's regularize.py:
 40-80), so the batch is partitioned across ranks into contiguous blocks with no
-data-path communication; inside a rank, plots run concurrently on several CUDA streams
-(each stream replays its own captured iteration graph on its own workspace), which
-fills the GPU with the small 1024^2 grid kernels of several plots at once.  One
-collective at the end gathers the final positions of every plot (NCCL all-gather over
-NVLink on GPUs; gloo in the CPU tests).
+data-path communication.  Inside a rank the block runs as ONE batched run
+(inim_run_batched): every stage of every iteration is a single launch over all plots
+with the plot index in grid.z, so the 1024^2 kernels of the whole block fill the GPU
+together, captured once into a CUDA graph and replayed.  One collective at the end
+gathers the final positions of every plot (NCCL all-gather over NVLink on GPUs; gloo
+in the CPU tests).
 
 The reference runs the same workload as a process pool over host cores
-(tests/test_acceptance.py:124-128).
+(tests/test_acceptance.py:107-128), one regularize.run per plot.
 """
 
 from __future__ import annotations
@@ -60,11 +61,12 @@ class SplomConfig:
     k: int = 10
     kernel_size: int = 8
     iterations: int = 10
-    streams: int = 8
+    max_batch: int = 256        # plots per batched launch (bounds the workspace: ~43 MB per plot at C4)
+    collect_metrics: bool = False  # per-frame binned_stddev / overplotting of every plot ("basic")
 
 
 class DeviceSplom:
-    """Runs this rank's block of plots on `streams` concurrent CUDA streams."""
+    """Runs this rank's block of plots as batched runs of up to `max_batch` plots."""
 
     def __init__(self, cfg: SplomConfig, plot_ids: Sequence[int], device=None):
         import torch
@@ -74,42 +76,51 @@ class DeviceSplom:
 
         self.torch, self.D, self._lib = torch, D, _lib
         self.lib = D.require_cuda()
+        D.check_grid(cfg.k)
         self.cfg = cfg
         self.ids = list(plot_ids)
         self.dev = device or D.device()
         n = cfg.points
-        self.inputs = torch.empty((len(self.ids), n, 2), dtype=torch.float32, device=self.dev)
+        nb = len(self.ids)
+        self.inputs = torch.empty((nb, n, 2), dtype=torch.float32, device=self.dev)
         self.work = torch.empty_like(self.inputs)
-        nst = max(1, min(cfg.streams, len(self.ids)))
-        self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(nst)]
-        wsb = int(self.lib.inim_workspace_bytes(cfg.k, n))
-        self.ws = [torch.empty(wsb, dtype=torch.uint8, device=self.dev) for _ in range(nst)]
+        # plots of an odd size cannot share 16-byte aligned batch strides: one per launch
+        self.batch = max(1, min(cfg.max_batch, nb)) if n % 2 == 0 else 1
+        wsb = int(self.lib.inim_workspace_bytes(cfg.k, n, self.batch))
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
+        self.stats = (torch.zeros((nb, cfg.iterations, 3), dtype=torch.int64, device=self.dev)
+                      if cfg.collect_metrics else None)
 
     def load(self, make_plot: Callable[[int], np.ndarray]):
         for q, idx in enumerate(self.ids):
             self.inputs[q].copy_(self.torch.from_numpy(make_plot(idx).astype(np.float32)))
 
     def run(self):
-        """All plots, `iterations` each; inputs stay untouched (results in .work)."""
-        torch, D, lib, cfg = self.torch, self.D, self.lib, self.cfg
-        cur = torch.cuda.current_stream(self.dev)
-        start = torch.cuda.Event()
-        start.record(cur)
-        for st in self.streams:
-            st.wait_event(start)
-        for q in range(len(self.ids)):
-            si = q % len(self.streams)
-            st = self.streams[si]
-            with torch.cuda.stream(st):
-                self.work[q].copy_(self.inputs[q])
-                self._lib.check(lib.inim_run(D.ptr(self.work[q]), cfg.points, cfg.k, cfg.kernel_size, 0.0,
-                                             cfg.iterations, 0.0, None, None, None, None, None,
-                                             D.ptr(self.ws[si]), st.cuda_stream), "splom run")
-        for st in self.streams:
-            ev = torch.cuda.Event()
-            ev.record(st)
-            cur.wait_event(ev)
+        """All plots, `iterations` each, on the current stream; inputs stay untouched
+        (results in .work)."""
+        D, lib, cfg = self.D, self.lib, self.cfg
+        self.work.copy_(self.inputs)
+        stream = D.stream()
+        for b0 in range(0, len(self.ids), self.batch):
+            b1 = min(b0 + self.batch, len(self.ids))
+            stats = D.ptr(self.stats[b0:b1]) if self.stats is not None else None
+            self._lib.check(lib.inim_run_batched(D.ptr(self.work[b0:b1]), cfg.points, b1 - b0, cfg.k,
+                                                 cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(self.ws),
+                                                 stream), "splom run")
         return self.work
+
+    def metrics(self):
+        """Per plot and frame 1..iterations: (binned_stddev, overplotting) as the
+        reference's record_for_frame (metrics.py:46-71, 147-168), from the device
+        occupancy statistics."""
+        from .metrics import overplotting_from_stats, stddev_from_stats
+
+        if self.stats is None:
+            raise ValueError("SplomConfig(collect_metrics=True) is needed")
+        st = self.stats.cpu().numpy()
+        n, k = self.cfg.points, self.cfg.k
+        return [[(stddev_from_stats(int(st[q, t, 1]), int(st[q, t, 2]), k), overplotting_from_stats(int(st[q, t, 0]), n))
+                 for t in range(self.cfg.iterations)] for q in range(len(self.ids))]
 
 
 def gather_results(local, nplots: int, world: int, group=None):

@@ -98,3 +98,45 @@ def test_max_over_ranks_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: 2.0, 1: 2.0}
+
+
+def test_bench_gpus2_self_launch_shard_gather_on_gloo():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with two ranks
+    (torch.distributed.run), each rank takes its contiguous block of the SPLOM batch,
+    runs it (compute stubbed on the CPU: --cpu-stub) and the step all-gathers every
+    plot's positions; rank 0 prints one line with n_gpus = 2 and the reassembled order
+    checked, the max-over-ranks timing in ms_per_step."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ)
+    for v in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(v, None)
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--cpu-stub", "--plots", "7",
+                          "--splom-points", "16", "--steps", "2", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=str(root))
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["scaling"] == "strong"
+    assert rec["collective"]["world"] == 2 and rec["collective"]["backend"] == "gloo"
+    assert rec["collective"]["gather_ok"] is True
+    assert rec["plots_per_rank"] == 4  # rank 0's block of 7 plots over 2 ranks
+    assert rec["value"] > 0 and rec["ms_per_step"] > 0
+
+
+def test_bench_rejects_mismatched_world():
+    """--gpus N under a torchrun world of a different size fails loudly."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--cpu-stub"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=str(root))
+    assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr

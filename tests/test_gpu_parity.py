@@ -388,18 +388,30 @@ def test_run_host_abi_end_to_end(P, oracle):
     assert maxerr(out, want) <= POS_TOL
 
 
-def test_splom_streams_match_single_plot_runs(P):
-    """SPLOM batch on concurrent streams == each plot regularized alone (bit-identical)."""
+@pytest.mark.parametrize("points,iters,max_batch", [(20_000, 4, 4), (70_000, 4, 3), (30_000, 2, 8)])
+def test_splom_batch_matches_single_plot_runs(P, points, iters, max_batch):
+    """A batched SPLOM run (inim_run_batched: plot index in grid.z) == each plot
+    regularized alone, bit for bit; with and without the per-run point sort (n >=
+    65,536 and >= 3 iterations), in chunks of max_batch plots; its per-plot frame
+    statistics equal run(collect_metrics="basic")'s."""
     from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
 
-    cfg = SplomConfig(nplots=6, points=20_000, k=8, kernel_size=8, iterations=4, streams=3)
+    cfg = SplomConfig(nplots=5, points=points, k=8, kernel_size=8, iterations=iters, max_batch=max_batch,
+                      collect_metrics=True)
     job = DeviceSplom(cfg, range(cfg.nplots))
     job.load(lambda i: splom_plot(i, cfg.points))
     res = job.run().cpu().numpy().astype(np.float64)
+    mets = job.metrics()
     for i in range(cfg.nplots):
         r = P.run(P.ScatterDataset(positions=splom_plot(i, cfg.points)),
-                  P.RegularizationParams(k=8, kernel_size=8, iterations=4), store_fields=False)
-        assert np.array_equal(res[i], r.frame(4)), i
+                  P.RegularizationParams(k=8, kernel_size=8, iterations=iters), collect_metrics="basic",
+                  store_fields=False)
+        assert np.array_equal(res[i], r.frame(iters)), i
+        for t in range(iters):
+            m = r.metrics[t + 1]
+            assert mets[i][t] == (m.binned_stddev, m.overplotting), (i, t)
+    again = job.run().cpu().numpy().astype(np.float64)  # graph replay: same answer
+    assert np.array_equal(again, res)
 
 
 @pytest.mark.parametrize("k", [11, 12])
@@ -438,7 +450,7 @@ def test_field_layouts_bit_identical(tmp_path, k):
             lib = _lib.load()
             host = np.load({str(tmp_path / "in.npy")!r})
             n = len(host)
-            ws = torch.empty(int(lib.inim_workspace_bytes({k}, n)), dtype=torch.uint8, device="cuda")
+            ws = torch.empty(int(lib.inim_workspace_bytes({k}, n, 1)), dtype=torch.uint8, device="cuda")
             a = torch.from_numpy(host).cuda()
             _lib.check(lib.inim_run_uncached(D.ptr(a), n, {k}, 8, 0.0, 4, 0.0, None, None, None, None, None,
                                              D.ptr(ws), D.stream()), "run")

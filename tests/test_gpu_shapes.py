@@ -116,16 +116,18 @@ def test_c3_bench_input_ten_iterations(P, oracle_mt):
 
 
 # ------------------------------------------------------------------------------ C4
-@pytest.mark.parametrize("idx", [0, 1, 2])
-def test_c4_splom_plot_against_oracle(P, oracle_mt, idx):
-    """BASELINE configs[3] plot shape: 500k points, 1024^2, 10 iterations."""
-    from paper_2408_06513_b200.splom import splom_plot
+def test_c4_splom_batch_against_oracle(P, oracle_mt):
+    """BASELINE configs[3] plot shape through the batched SPLOM path: 3 plots of 500k
+    points, 1024^2, 10 iterations, one batched run, each plot against the oracle."""
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
 
-    pts = splom_plot(idx, 500_000)
-    want = oracle_frames(oracle_mt, pts, 10, 8, 10, {10})
-    r = P.run(P.ScatterDataset(positions=pts), P.RegularizationParams(k=10, kernel_size=8, iterations=10),
-              store_fields=False)
-    assert maxerr(r.frame(10), want[10]) <= POS_TOL
+    cfg = SplomConfig(nplots=3, points=500_000, k=10, kernel_size=8, iterations=10)
+    job = DeviceSplom(cfg, range(cfg.nplots))
+    job.load(lambda i: splom_plot(i, cfg.points))
+    res = job.run().cpu().numpy().astype(np.float64)
+    for i in range(cfg.nplots):
+        want = oracle_frames(oracle_mt, splom_plot(i, cfg.points), 10, 8, 10, {10})
+        assert maxerr(res[i], want[10]) <= POS_TOL, i
 
 
 # ------------------------------------------------------------------------------ C5
@@ -143,8 +145,8 @@ class DeviceBrute:
     def _rows(self, lo, hi):
         """sum over rows j' of d[j', lo[j']..hi[j']] (inclusive, clipped; empty if lo > hi)."""
         torch, s, P = self.torch, self.s, self.P
-        lo = lo.clamp(min=0)
-        hi = hi.clamp(max=s - 1)
+        lo = lo.clamp(0, s)
+        hi = hi.clamp(-1, s - 1)
         ok = lo <= hi
         hi_c = hi.clamp(min=0)
         top = P.gather(1, hi_c[:, None])[:, 0]
@@ -220,7 +222,7 @@ def device_tables(P, d, k):
     s = 1 << k
     tables = torch.empty((8, s, s), dtype=torch.float32, device=d.device)
     total = torch.empty(1, dtype=torch.float64, device=d.device)
-    ws = torch.empty(int(lib.inim_workspace_bytes(k, 0)), dtype=torch.uint8, device=d.device)
+    ws = torch.empty(int(lib.inim_workspace_bytes(k, 0, 1)), dtype=torch.uint8, device=d.device)
     _lib.check(lib.inim_integral_set(D.ptr(d), k, D.ptr(tables), D.ptr(total), D.ptr(ws), D.stream()), "integral")
     del ws
     return tables, float(total.item())
@@ -289,7 +291,7 @@ def test_field_large_grids_at_spot_pixels(P, k):
     targets = torch.empty((s, s, 2), dtype=torch.float32, device="cuda")
     exc = torch.zeros(1, dtype=torch.float32, device="cuda")
     total = torch.empty(1, dtype=torch.float64, device="cuda")
-    ws = torch.empty(int(lib.inim_workspace_bytes(k, 0)), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(int(lib.inim_workspace_bytes(k, 0, 1)), dtype=torch.uint8, device="cuda")
     _lib.check(lib.inim_field_from_density(D.ptr(d), k, None, D.ptr(targets), D.ptr(exc), D.ptr(total), D.ptr(ws),
                                            D.stream()), "field")
     del ws

@@ -33,7 +33,7 @@ def main():
             host, k = four_cluster(), 10
         n = len(host)
         pts = torch.from_numpy(host.astype(np.float32)).to(dev)
-        ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev)
+        ws = torch.empty(int(lib.inim_workspace_bytes(k, n, 1)), dtype=torch.uint8, device=dev)
         for _ in range(2):
             _lib.check(lib.inim_run_uncached(D.ptr(pts), n, k, 8, 0.0, ITER, 0.0, None, None, None, None, None,
                                              D.ptr(ws), D.stream()), "run")
@@ -44,7 +44,7 @@ def main():
             d = torch.rand((s, s), device=dev) * 10
             t8 = torch.empty((8, s, s), device=dev)
             tot = torch.empty(1, dtype=torch.float64, device=dev)
-            ws = torch.empty(int(lib.inim_workspace_bytes(k, 0)), dtype=torch.uint8, device=dev)
+            ws = torch.empty(int(lib.inim_workspace_bytes(k, 0, 1)), dtype=torch.uint8, device=dev)
             for _ in range(2):
                 _lib.check(lib.inim_integral_set(D.ptr(d), k, D.ptr(t8), D.ptr(tot), D.ptr(ws), D.stream()), "int")
     torch.cuda.synchronize()

@@ -19,7 +19,7 @@ host, k = (c3_points(16_000_000), 12) if big else (four_cluster(), 10)
 n = len(host)
 pin = torch.from_numpy(host.astype(np.float32)).to(dev)
 pts = torch.empty_like(pin)
-ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device=dev)
+ws = torch.empty(int(lib.inim_workspace_bytes(k, n, 1)), dtype=torch.uint8, device=dev)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 st = D.stream()
 rows = []

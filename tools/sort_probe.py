@@ -27,7 +27,7 @@ def profile(lib, host, k, iters=10, reps=3):
     n = len(host)
     pts0 = torch.from_numpy(host.astype(np.float32)).cuda()
     pts = pts0.clone()
-    ws = torch.empty(int(lib.inim_workspace_bytes(k, n)), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(int(lib.inim_workspace_bytes(k, n, 1)), dtype=torch.uint8, device="cuda")
     cap = 64 * iters
     ms = (ctypes.c_float * cap)()
     names = ctypes.create_string_buffer(cap * 24)
