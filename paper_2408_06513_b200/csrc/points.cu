@@ -84,14 +84,16 @@ __device__ __forceinline__ void move_point(const float* tg, int s, float x, floa
     else bilinear<float>(reinterpret_cast<const float2*>(tg), s, x, y, ox, oy);
 }
 
-template <bool PAIRS, int U>
-__global__ void __launch_bounds__(256, 5) sample_f32_kernel(const float* __restrict__ tg, int k,
+// BATCH: plot offsets of a SPLOM batch (grid.z), a separate instantiation so the
+// single-plot move keeps its register budget.
+template <bool PAIRS, int U, bool BATCH>
+__global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict__ tg, int k,
                                                          const float* __restrict__ in, float* __restrict__ out,
                                                          int64_t n, int clip, float* max_disp, const int* state,
                                                          uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
                                                          int agg, int64_t zin, int64_t zout, int64_t zslab) {
     pdl_enter();
-    {  // plot blockIdx.z of a batch
+    if (BATCH) {  // plot blockIdx.z of a batch
         const int64_t zo = zslab_off(zslab);
         tg = zoff(tg, zo);
         in += blockIdx.z * zin;
@@ -494,7 +496,8 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
     const int64_t npair = n >> 1;
     // two point pairs (two 16-byte loads) per thread per step (measured: 1 or 4 are
     // slower at C2)
-    auto kern = pairs ? sample_f32_kernel<true, 2> : sample_f32_kernel<false, 2>;
+    auto kern = bt.B > 1 ? (pairs ? sample_f32_kernel<true, 2, true> : sample_f32_kernel<false, 2, true>)
+                         : (pairs ? sample_f32_kernel<true, 2, false> : sample_f32_kernel<false, 2, false>);
     const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair, 256 * 2, bt);
     INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, in, out, n, clip, max_disp, state, splat_next, zn0,
                              zn1, sorted ? 1 : 0, zin, zout, bt.slab));

@@ -343,7 +343,8 @@ def test_run_largest_grid_against_staged_path(P):
 def test_density_generic_kernel_sizes(P, oracle, ks):
     pts = clusters(200_000, 3)
     tex = P.build_density(pts, P.RegularizationParams(k=9, kernel_size=ks))
-    want = oracle.build_density(pts, 9, ks)
+    want, bg = oracle.build_density(pts, 9, ks)
+    assert tex.background == bg
     assert maxerr(tex.values, want) <= 2e-6 * want.max()
 
 
