@@ -293,9 +293,10 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         const bool splat_next = more || (fstats && key.n > 0);
         const Chain chain{t > 0 || sorted, splat_next, more ? exc_at(t + 1) : nullptr,
                           more ? disp_at(t + 1) : nullptr, sorted};
-        // the move reads the paired field layout (two 16-byte gathers per point) unless
-        // INIM_PAIRS=0 (the plain (s, s, 2) layout: half the field bytes, four gathers)
-        const bool pairs = use_pairs(g);
+        // the move reads the paired field layout (two 16-byte gathers per point) while the
+        // field stays L2-resident: one plot up to 2048^2 (INIM_PAIRS overrides); a batch's
+        // fields stream through HBM, where the plain (s, s, 2) layout's half bytes win
+        const bool pairs = use_pairs(g) && B == 1;
         float* plain = tg ? tg : (pairs ? nullptr : tg_scratch);
         int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, plain, exc_at(t),
                                    disp_at(t), key.eps, state, w, mp, st, pairs ? tg_scratch : nullptr, chain, bt,

@@ -370,160 +370,4 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     __syncthreads();
 }
 
-// ------------------------------------------------------------ fused h + v + reduce
-// One CTA = one VR x TW tile of d (TW = the integral tile width, 32 CPL; VR = 64 rows,
-// VB bands).  The horizontal pass runs on the VR + 2R rows the vertical pass needs
-// (the vertical halo is recomputed by both neighbouring CTAs: (VR + 2R) / VR horizontal
-// work), straight from the counts: 32-row chunks of the input are staged in shared
-// memory (the next chunk's loads in flight in registers while the current one is
-// filtered), each lane filters one row of the chunk, each warp a TW / 8 column chunk,
-// and the outputs land in the tile buffer `hs` ((VR + 2R) x TWP, padded rows: the
-// lane-per-row float4 stores are conflict-free).  Then the vertical pass in place
-// (fir_cols4_inplace), the tile reduce of every band straight from shared memory, and
-// the d store.  Compared with the two-kernel path this drops the 4 B/px write and
-// ~7 B/px re-read of the horizontal scratch and one launch.
-constexpr int kFusedRows = 64;   // VR
-constexpr int kFusedChunk = 32;  // staged input rows per chunk (one per lane)
-
-template <int CPL>
-struct Fused {
-    static constexpr int TW = 32 * CPL;
-    static constexpr int TWP = TW + 4;     // hs row pitch (floats)
-    static constexpr int CW = TW / 8;      // h-pass outputs per lane (8 warps)
-    static constexpr int THREADS = 256;
-};
-
-__host__ __device__ inline int fused_pitch(int TW, int R) {  // staging pitch: >= TW + 2R + 3, pitch / 4 odd
-    int p = (TW + 2 * R + 3 + 3) & ~3;
-    if (((p >> 2) & 1) == 0) p += 4;
-    return p;
-}
-
-__host__ __device__ inline size_t fused_smem_bytes(int TW, int R) {
-    return ((size_t)(kFusedRows + 2 * R) * (TW + 4) + (size_t)kFusedChunk * fused_pitch(TW, R)) * sizeof(float);
-}
-
-template <int R, int CPL, typename T>
-__device__ __forceinline__ void smooth_fused_tile(const T* __restrict__ in, float* __restrict__ d,
-                                                  uint32_t* __restrict__ zero_next, const Geo& g, const Ws& ws,
-                                                  float background, int emit, int bx, int by, float* sm) {
-    using F = Fused<CPL>;
-    constexpr int TW = F::TW, TWP = F::TWP, CW = F::CW, CR = kFusedChunk, VR = kFusedRows;
-    constexpr int H = VR + 2 * R;           // rows of the horizontal pass
-    constexpr int NCH = (H + CR - 1) / CR;  // staged chunks
-    constexpr bool VEC = (R & 3) == 0;      // (i0 - R) is a multiple of 4: 16-byte staging loads
-    constexpr int W4 = (TW + 2 * R + 3) / 4;                           // 16-byte groups per staged row
-    constexpr int PF = (CR * W4 + F::THREADS - 1) / F::THREADS;        // prefetch slots per thread
-    const int s = g.s, TH = g.TH;
-    const int a0 = by * VR, i0 = bx * TW;
-    const int ld = fused_pitch(TW, R);
-    float* hs = sm;                          // [H][TWP]
-    float* st = sm + (size_t)H * TWP;        // [CR][ld]
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const bool colint = i0 - R >= 0 && i0 + TW + R <= s;
-    const bool vec = VEC && colint;
-    if (zero_next) {  // this tile's VR x TW block of the next count buffer
-        constexpr int TW4 = TW / 4;
-        for (int q = tid; q < VR * TW4; q += F::THREADS) {
-            const int r = q / TW4, c4 = q - r * TW4;
-            reinterpret_cast<uint4*>(zero_next + (int64_t)(a0 + r) * s + i0)[c4] = make_uint4(0u, 0u, 0u, 0u);
-        }
-    }
-    // ---- horizontal pass, chunk by chunk
-    uint4 pf[PF];
-    auto issue = [&](int c) {  // vec: the chunk's 16-byte groups into registers
-#pragma unroll
-        for (int j = 0; j < PF; ++j) {
-            const int q = tid + j * F::THREADS;
-            const int rr = q / W4, c4 = q - rr * W4;
-            const int r = c * CR + rr;
-            if (q < CR * W4 && r < H) {
-                const int row = reflect_index(a0 - R + r, s);
-                pf[j] = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(in) + (int64_t)row * s +
-                                                             i0 - R) + c4);
-            }
-        }
-    };
-    auto place = [&](int c) {  // registers (vec) or global (border tiles) -> staging rows
-        if (vec) {
-#pragma unroll
-            for (int j = 0; j < PF; ++j) {
-                const int q = tid + j * F::THREADS;
-                const int rr = q / W4, c4 = q - rr * W4;
-                if (q < CR * W4 && c * CR + rr < H) {
-                    const uint4 u = pf[j];
-                    float4 f;
-                    if (std::is_same<T, float>::value)
-                        f = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
-                                        __uint_as_float(u.w));
-                    else
-                        f = make_float4((float)u.x, (float)u.y, (float)u.z, (float)u.w);
-                    *reinterpret_cast<float4*>(st + rr * ld + 4 * c4) = f;
-                }
-            }
-        } else {
-            const int Wc = TW + 2 * R;
-            for (int q = tid; q < CR * Wc; q += F::THREADS) {
-                const int rr = q / Wc, cc = q - rr * Wc;
-                const int r = c * CR + rr;
-                if (r < H) {
-                    const int row = reflect_index(a0 - R + r, s);
-                    st[rr * ld + cc] = (float)__ldg(in + (int64_t)row * s + reflect_index(i0 - R + cc, s));
-                }
-            }
-        }
-    };
-    if (vec) issue(0);
-#pragma unroll 1
-    for (int c = 0; c < NCH; ++c) {
-        place(c);
-        __syncthreads();
-        if (vec && c + 1 < NCH) issue(c + 1);  // in flight while this chunk is filtered
-        const int r = c * CR + lane;
-        if (r < H) {
-            const float* row = st + lane * ld + w * CW;
-            float acc[CW];
-#pragma unroll
-            for (int p = 0; p < CW; ++p) acc[p] = 0.f;
-            constexpr int NT = 2 * R + 1;
-            constexpr int NQ = CW + NT - 1;
-#pragma unroll
-            for (int q4 = 0; q4 < (NQ + 3) / 4; ++q4) {
-                const float4 v4 = *reinterpret_cast<const float4*>(row + 4 * q4);
-                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int q = 4 * q4 + e;
-#pragma unroll
-                    for (int p = 0; p < CW; ++p) {
-                        const int t = q - p;
-                        if (q < NQ && t >= 0 && t < NT) acc[p] = fmaf(TapsOf<R / 3>::w(t), vv[e], acc[p]);
-                    }
-                }
-            }
-            float4* dst = reinterpret_cast<float4*>(hs + (size_t)r * TWP + w * CW);
-#pragma unroll
-            for (int p = 0; p < CW / 4; ++p)
-                dst[p] = make_float4(acc[4 * p], acc[4 * p + 1], acc[4 * p + 2], acc[4 * p + 3]);
-        }
-        __syncthreads();  // the staging rows are refilled next
-    }
-    // ---- vertical pass in place: thread = (band group, column quad), P = TH / 4 rows
-    const int GT = TW;  // threads per band
-    const int grp = tid / GT, t = tid - grp * GT;
-    const int VB = VR / TH;
-    if (TH == 32) fir_cols4_inplace<R, 8>(hs, TW, grp * TH, t, grp < VB, background, TWP);
-    else fir_cols4_inplace<R, 4>(hs, TW, grp * TH, t, grp < VB, background, TWP);
-    __syncthreads();
-    if (emit) {  // the tile reduce of every band, straight from shared memory
-        for (int gb = w; gb < VB; gb += F::THREADS / 32)
-            warp_tile_reduce<CPL>(hs + (size_t)gb * TH * TWP, TWP, g, ws, a0 / TH + gb, bx, lane);
-    }
-    constexpr int TW4 = TW / 4;
-    for (int q = tid; q < VR * TW4; q += F::THREADS) {
-        const int r = q / TW4, c4 = q - r * TW4;
-        reinterpret_cast<float4*>(d + (int64_t)(a0 + r) * s + i0)[c4] = *reinterpret_cast<const float4*>(hs + r * TWP + 4 * c4);
-    }
-}
-
 }  // namespace inim

@@ -10,8 +10,6 @@
 
 namespace inim {
 
-bool fused_enabled();  // smooth.cu: INIM_FUSED_SMOOTH=0 selects the two-kernel path
-
 template <int R, typename T>
 __global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
@@ -38,33 +36,6 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
     const int64_t zo = zslab_off(zslab);
     smooth_v_tile<R>(zoff(tmp, zo), zoff(d, zo), g, v, ws_shift(ws, zo), taps, background, emit, blockIdx.x,
                      blockIdx.y, vsm);
-}
-
-// Fused horizontal + vertical pass + tile reduce (inim_smooth.cuh smooth_fused_tile):
-// the iteration's smoothing of the counts in one launch.
-template <int R, int CPL>
-__global__ void __launch_bounds__(256) smooth_fused_kernel(const uint32_t* __restrict__ in, float* __restrict__ d,
-                                                           uint32_t* __restrict__ zero_next, const Geo g, const Ws ws,
-                                                           float background, int emit, const int* state,
-                                                           int64_t zslab) {
-    pdl_enter();
-    if (state && state[0]) return;
-    extern __shared__ __align__(16) float fsm[];
-    const int64_t zo = zslab_off(zslab);  // plot blockIdx.z of a batch
-    smooth_fused_tile<R, CPL, uint32_t>(zoff(in, zo), zoff(d, zo), zoff_opt(zero_next, zo), g, ws_shift(ws, zo),
-                                        background, emit, blockIdx.x, blockIdx.y, fsm);
-}
-
-template <int R, int CPL>
-inline int launch_fused(const uint32_t* counts, float* d, uint32_t* zero_next, const Geo& g, const Ws& ws, float bg,
-                        int emit, const int* state, cudaStream_t st, const Bat& bt) {
-    const size_t smem = fused_smem_bytes(g.TW, R);
-    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_fused_kernel<R, CPL>, (int)smem));
-    const dim3 grid(g.NX, g.s / kFusedRows, bt.B);
-    INIM_CUDA_TRY(launch_pdl(smooth_fused_kernel<R, CPL>, grid, dim3(Fused<CPL>::THREADS), smem, st, counts, d,
-                             zero_next, g, ws, bg, emit, state, bt.slab));
-    prof_mark(st, emit ? "smooth_fused_reduce" : "smooth_fused");
-    return (int)cudaGetLastError();
 }
 
 template <int R, typename T>
@@ -98,12 +69,6 @@ template <int KS>
 int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt) {
     constexpr int R = 3 * KS;
-    // the counts of the iteration (grids of 64^2 and up): one fused launch
-    if (counts && g.s >= kFusedRows && fused_enabled()) {
-        const uint32_t* c = static_cast<const uint32_t*>(in);
-        if (g.CPL == 4) return launch_fused<R, 4>(c, d, zero_next, g, ws, bg, emit, state, st, bt);
-        if (g.CPL == 2) return launch_fused<R, 2>(c, d, zero_next, g, ws, bg, emit, state, st, bt);
-    }
     int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st,
                                             bt)
                     : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st, bt);

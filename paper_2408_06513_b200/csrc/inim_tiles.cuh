@@ -1,5 +1,5 @@
 // Warp-per-tile integral kernels (phase 1 reduce, phase 3 write), shared by the
-// standalone integral kernels (integral.cu) and the fused smoothing kernel (smooth.cu).
+// standalone integral kernels (integral.cu) and the vertical smoothing pass (smooth.cu).
 //
 // One warp owns one TH x TW tile (TW = 32 * CPL, TH <= 32); lane l owns the CPL
 // consecutive columns 4l..4l+3 (CPL = 4) and sweeps the TH rows.  Nothing crosses a

@@ -88,8 +88,9 @@ __device__ __forceinline__ void move_point(const float* tg, int s, float x, floa
 // single-plot move keeps its register budget.
 template <bool PAIRS, int U, bool BATCH>
 __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict__ tg, int k,
-                                                         const float* __restrict__ in, float* __restrict__ out,
-                                                         int64_t n, int clip, float* max_disp, const int* state,
+                                                         const float4* __restrict__ in2, const float* __restrict__ in,
+                                                         float4* __restrict__ out2, float* __restrict__ out, int64_t n,
+                                                         int clip, float* max_disp, const int* state,
                                                          uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
                                                          int agg, int64_t zin, int64_t zout, int64_t zslab) {
     pdl_enter();
@@ -98,13 +99,13 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
         tg = zoff(tg, zo);
         in += blockIdx.z * zin;
         out += blockIdx.z * zout;
+        in2 = reinterpret_cast<const float4*>(in);
+        out2 = reinterpret_cast<float4*>(out);
         max_disp = zoff_opt(max_disp, zo);
         splat_next = zoff_opt(splat_next, zo);
         zn0 = zoff_opt(zn0, zo);
         zn1 = zoff_opt(zn1, zo);
     }
-    const float4* __restrict__ in2 = reinterpret_cast<const float4*>(in);
-    float4* __restrict__ out2 = reinterpret_cast<float4*>(out);
     const bool stopped = state && state[0];
     const int s = 1 << k;
     // fused splat of the next iteration (its count buffer was cleared by this
@@ -499,8 +500,9 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
     auto kern = bt.B > 1 ? (pairs ? sample_f32_kernel<true, 2, true> : sample_f32_kernel<false, 2, true>)
                          : (pairs ? sample_f32_kernel<true, 2, false> : sample_f32_kernel<false, 2, false>);
     const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair, 256 * 2, bt);
-    INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, in, out, n, clip, max_disp, state, splat_next, zn0,
-                             zn1, sorted ? 1 : 0, zin, zout, bt.slab));
+    INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, reinterpret_cast<const float4*>(in), in,
+                             reinterpret_cast<float4*>(out), out, n, clip, max_disp, state, splat_next, zn0, zn1,
+                             sorted ? 1 : 0, zin, zout, bt.slab));
     prof_mark(st, "sample");
     return (int)cudaGetLastError();
 }

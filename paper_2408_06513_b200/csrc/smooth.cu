@@ -11,21 +11,8 @@
 
 namespace inim {
 
-// INIM_FUSED_SMOOTH=1: the fused smoothing kernel (one launch, no horizontal-pass
-// scratch) instead of the two-kernel path.  Off by default: measured slower at C2, C3
-// and the SPLOM batch, the recomputed vertical halo costs more FFMA
-// issue than the scratch round trip saves.
-bool fused_enabled() {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = getenv("INIM_FUSED_SMOOTH");
-        env = (e && e[0] == '1') ? 1 : 0;
-    }
-    return env == 1;
-}
-
 // ------------------------------------------------------- generic taps (kernel_size > 16)
-// The compiled FIRs above carry the taps of kernel_size 1..16 as FFMA immediates.  Any
+// The compiled FIRs carry the taps of kernel_size 1..16 as FFMA immediates.  Any
 // larger kernel (the reference accepts every kernel_size >= 1, density.py:40-51) runs
 // these runtime-tap kernels: the taps are evaluated on the device in float64 (the same
 // exp / sum as smoothing_kernel, the sum passed in from the host) and stored float32.

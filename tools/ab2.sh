@@ -1,0 +1,11 @@
+#!/bin/bash
+# A/B of libinim builds on one box (run under gpurun): C2 and C3 graph-replay slopes,
+# interleaved, each build twice.   bash tools/ab2.sh ab/libA.so ab/libB.so ...
+for rep in 1 2; do
+  for L in "$@"; do
+    echo "$L c2 $(INIM_LIB_PATH=$L python tools/run_probe.py | tail -1)"
+  done
+done
+for L in "$@"; do
+  echo "$L c3 $(INIM_LIB_PATH=$L python tools/run_probe.py c3 | tail -1)"
+done

@@ -2,6 +2,7 @@
 
   python tools/prof_driver.py iter       # 2 eager iterations of the 1M / 1024^2 workload
   python tools/prof_driver.py integral   # inim_integral_set at 4096^2 (and 16384^2 with --big)
+  python tools/prof_driver.py splom      # a batched SPLOM run (PROF_PLOTS plots, PROF_ITERS iterations)
 """
 
 import os
@@ -37,6 +38,15 @@ def main():
         for _ in range(2):
             _lib.check(lib.inim_run_uncached(D.ptr(pts), n, k, 8, 0.0, ITER, 0.0, None, None, None, None, None,
                                              D.ptr(ws), D.stream()), "run")
+    elif mode == "splom":  # one batched run of PROF_PLOTS C4 plots (500k points, 1024^2)
+        from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
+
+        nplots = int(os.environ.get("PROF_PLOTS", "32"))
+        cfg = SplomConfig(nplots=nplots, points=500_000, k=10, kernel_size=8, iterations=ITER)
+        job = DeviceSplom(cfg, range(nplots))
+        job.load(lambda i: splom_plot(i % 8, cfg.points))
+        for _ in range(2):
+            job.run()
     else:
         ks = [12] + ([14] if "--big" in sys.argv else [])
         for k in ks:
