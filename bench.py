@@ -527,7 +527,8 @@ def splom_job(args, world: int, rank: int, device_stub: bool):
     points = args.splom_points
     if device_stub:
         return _StubSplom(ids, points), ids
-    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS)
+    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS,
+                      streams=args.splom_streams)
     job = DeviceSplom(cfg, ids)
     job.load(lambda i: splom_plot(i, points))
     return job, ids
@@ -634,8 +635,7 @@ def job_launches(job) -> int:
     """Kernels per SPLOM step: per batched run, the splat, the point sort (3 scan kernels
     + placement), six kernels per iteration and the final unpermute (+ the counts
     memset node, not a kernel)."""
-    runs = -(-len(job.ids) // job.batch)
-    return runs * (1 + 4 + 6 * ITERS + 1)
+    return len(job.chunks) * (1 + 4 + 6 * ITERS + 1)
 
 
 def splom_e2e(args, job, world, dist):
@@ -732,6 +732,7 @@ def main():
                          "c3: 16M pts/4096^2; sweep: integral-only 512^2..16384^2")
     ap.add_argument("--plots", type=int, default=256)
     ap.add_argument("--splom-points", type=int, default=SPLOM_POINTS)
+    ap.add_argument("--splom-streams", type=int, default=1, help="concurrent sub-batches per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-splom", action="store_true", help="N = 1: leave the SPLOM batch out of the C2 line")
     ap.add_argument("--cpu-stub", action="store_true", help="multi-rank plumbing on gloo, no GPU (tests)")

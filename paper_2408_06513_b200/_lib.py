@@ -104,7 +104,10 @@ def load(path: Path | None = None):
         raise RuntimeError(f"libinim.so not built ({p}); run paper_2408_06513_b200._lib.build() "
                            "or `make -C paper_2408_06513_b200/csrc` -- there is no CPU fallback")
     lib = ctypes.CDLL(str(p))
+    alt = p.resolve() != LIB_PATH.resolve()
     for name, (res, args) in _SIGS.items():
+        if alt and not hasattr(lib, name):  # an older build under A/B timing: bind what it has
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
