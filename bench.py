@@ -527,8 +527,7 @@ def splom_job(args, world: int, rank: int, device_stub: bool):
     points = args.splom_points
     if device_stub:
         return _StubSplom(ids, points), ids
-    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS,
-                      streams=args.splom_streams)
+    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS)
     job = DeviceSplom(cfg, ids)
     job.load(lambda i: splom_plot(i, points))
     return job, ids
@@ -732,7 +731,6 @@ def main():
                          "c3: 16M pts/4096^2; sweep: integral-only 512^2..16384^2")
     ap.add_argument("--plots", type=int, default=256)
     ap.add_argument("--splom-points", type=int, default=SPLOM_POINTS)
-    ap.add_argument("--splom-streams", type=int, default=1, help="concurrent sub-batches per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-splom", action="store_true", help="N = 1: leave the SPLOM batch out of the C2 line")
     ap.add_argument("--cpu-stub", action="store_true", help="multi-rank plumbing on gloo, no GPU (tests)")

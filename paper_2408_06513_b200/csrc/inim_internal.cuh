@@ -36,7 +36,7 @@ inline cudaError_t ensure_smem_limit(const void* kernel, int bytes) {
 
 struct Geo {
     int k, s, TH, TW, B, NX, NW, WL, CPL;  // WL = lanes holding columns; CPL = columns per lane
-    int twlog, thlog;                      // log2(TW), log2(TH)
+    int twlog;                             // log2(TW)
     int64_t m;
 };
 
@@ -58,8 +58,6 @@ inline Geo make_geo(int k) {
     g.WL = g.TW >= 32 ? 32 : g.TW;
     g.twlog = 0;
     while ((1 << g.twlog) < g.TW) ++g.twlog;
-    g.thlog = 0;
-    while ((1 << g.thlog) < g.TH) ++g.thlog;
     return g;
 }
 
@@ -79,10 +77,9 @@ struct WsLayout {
     size_t tlcar;    // float [B+1][s]         rect_tl at the row above each band (row s-1 for b=B)
     size_t x1;       // float [B+1][s]         ULcar - TLcar (row B: along the last row)
     size_t x2;       // float [B+1][s+TH]      URcar + TLcar[c-1], extended with TLcar[s-1]
-    size_t hc;       // double [s][NX]         VH: in-band column scan of HC (row prefix of d up to each tile's first column)
+    size_t hc;       // double [s][NX]         row prefix of d up to each tile's first column
     size_t rpre;     // double [s]             in-band inclusive prefix of the row totals
     size_t taps;     // float [2s]             runtime taps of the generic smoothing (kernel_size > 16)
-    size_t marg;     // float [6][2s]          diagonal marginals Apre, Dsuf: raw, flat-folded, normalised (chains)
     size_t total;    // double [1]
     size_t misc;     // float [16]             scratch scalars
     size_t bytes;
@@ -116,7 +113,6 @@ inline WsLayout make_layout(const Geo& g) {
     L.hc = take(sizeof(double) * s * NX);
     L.rpre = take(sizeof(double) * s);
     L.taps = take(sizeof(float) * 2 * s);
-    L.marg = take(sizeof(float) * 12 * s);
     L.total = take(sizeof(double));
     L.misc = take(sizeof(float) * 16);
     L.bytes = o;
@@ -142,7 +138,6 @@ struct Ws {
     double* hc;
     double* rpre;
     float* taps;
-    float* marg;
     double* total;
     float* misc;
 };
@@ -167,7 +162,6 @@ inline Ws make_ws(void* base, const WsLayout& L) {
     w.hc = reinterpret_cast<double*>(b + L.hc);
     w.rpre = reinterpret_cast<double*>(b + L.rpre);
     w.taps = reinterpret_cast<float*>(b + L.taps);
-    w.marg = reinterpret_cast<float*>(b + L.marg);
     w.total = reinterpret_cast<double*>(b + L.total);
     w.misc = reinterpret_cast<float*>(b + L.misc);
     return w;
@@ -213,7 +207,6 @@ __host__ __device__ __forceinline__ Ws ws_shift(Ws w, int64_t b) {
     w.hc = zoff(w.hc, b);
     w.rpre = zoff(w.rpre, b);
     w.taps = zoff(w.taps, b);
-    w.marg = zoff(w.marg, b);
     w.total = zoff(w.total, b);
     w.misc = zoff(w.misc, b);
     return w;

@@ -315,10 +315,31 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
     const float* __restrict__ cpre = ws.tlcar + (int64_t)B * s;
     const float* __restrict__ x1 = ws.x1 + (int64_t)b * s;
     const float* __restrict__ x2 = ws.x2 + (int64_t)b * (s + TH);
-    // diagonal marginals, read off the chain carries by the chain scan (scan.cu
-    // chain_marginal): Apre[sigma] = Am[sigma], Dsuf[delta] = Dm[delta], in this mode's form
-    const float* __restrict__ Am = ws.marg + (size_t)4 * MODE * s;
-    const float* __restrict__ Dm = ws.marg + (size_t)(4 * MODE + 2) * s + (s - 1);
+    // diagonal marginals read off the chain carries (inim_scan.cuh "marg")
+    auto apre = [&](int sg) -> double {  // Apre[sigma]
+        if (sg < s) {
+            const int bb = sg / TH, r = sg - bb * TH;
+            return (double)ws.ure[(int64_t)bb * NX * TH + r] + (double)ws.x2[(int64_t)bb * (s + TH) + r + 1];
+        }
+        return (double)ws.x2[(int64_t)B * (s + TH) + sg - (s - 1)];
+    };
+    auto dsuf = [&](int dl) -> double {  // Dsuf[delta]
+        if (dl >= 0) {
+            const int j = s - 1 - dl, bb = j / TH, r = j - bb * TH, c2 = s - 2 - r;
+            return (double)ws.ule[((int64_t)bb * NX + NX - 1) * TH + r] + bandpre[bb] +
+                   (c2 >= 0 ? (double)ws.x1[(int64_t)bb * s + c2] : 0.0);
+        }
+        return (double)ws.x1[(int64_t)B * s + s - 1 + dl] + C;
+    };
+    // normalised marginal entries (MODE 1): value / C, minus the flat value when folding
+    auto nap = [&](int sg) {
+        const double v = apre(sg) * invC;
+        return (float)(diff ? v - (double)flat_apre_count(sg, s) * inv_s2 : v);
+    };
+    auto nds = [&](int dl) {
+        const double v = dsuf(dl) * invC;
+        return (float)(diff ? v - (double)flat_dsuf_count(dl, s) * inv_s2 : v);
+    };
     // per-column constants and initial windows (row 0)
     float A[CPL], Bc[CPL], w1[CPL], w2[CPL], wa[CPL], wd[CPL];
 #pragma unroll
@@ -329,16 +350,23 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         A[e] = (float)tv;
         w1[e] = (float)(ok && i - 1 >= 0 ? x1[i - 1] : 0.0);  // X1[i - r - 1]
         w2[e] = (float)(ok ? x2[i + 1] : 0.0);                // X2[i + r + 1]
-        Bc[e] = MODE == 0 ? (float)(cv - tv) : (float)(diff ? cv * invC - (i + 1) * inv_s : cv * invC);  // Cp
-        wa[e] = ok ? Am[a + i] : 0.f;  // Apre[i + j]
-        wd[e] = ok ? Dm[i - a] : 0.f;  // Dsuf[i - j]
+        if (MODE == 0) {
+            Bc[e] = (float)(cv - tv);
+            wa[e] = (float)(ok ? apre(a + i) : 0.0);  // Apre[i + j]
+            wd[e] = (float)(ok ? dsuf(i - a) : 0.0);  // Dsuf[i - j]
+        } else {
+            Bc[e] = (float)(diff ? cv * invC - (i + 1) * inv_s : cv * invC);  // Cp
+            wa[e] = ok ? nap(a + i) : 0.f;
+            wd[e] = ok ? nds(i - a) : 0.f;
+        }
     }
     // lane-distributed: row constants (lane q = row q) and window / chain edge entries
     float P = 0, Q = 0, S = 0;
     float e1 = 0, e2 = 0, ea = 0, ed = 0;
     float ulel = 0.f, urer = 0.f;
     {
-        const double vh = lane < TH ? ws.hc[(int64_t)(a + lane) * NX + x] : 0.0;  // VH (lines_kernel)
+        const double hc = lane < TH ? ws.hc[(int64_t)(a + lane) * NX + x] : 0.0;
+        const double vh = warp_inclusive_scan_d(hc, lane);
         if (lane < TH) {
             const double Rp = bandpre[b] + ws.rpre[a + lane];
             P = (float)vh;
@@ -352,8 +380,8 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                 const int c1 = i0 - 2 - lane;
                 e1 = (float)(c1 >= 0 ? x1[c1] : 0.0);
                 e2 = (float)x2[i0 + TW + 1 + lane];
-                ea = Am[a + i0 + TW + lane];
-                ed = Dm[i0 - a - 1 - lane];
+                ea = MODE == 0 ? (float)apre(a + i0 + TW + lane) : nap(a + i0 + TW + lane);
+                ed = MODE == 0 ? (float)dsuf(i0 - a - 1 - lane) : nds(i0 - a - 1 - lane);
             }
             ulel = x > 0 ? ws.ule[(tile - 1) * TH + lane] : 0.f;
             urer = x < NX - 1 ? ws.ure[(tile + 1) * TH + lane] : 0.f;

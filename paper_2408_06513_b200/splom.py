@@ -16,7 +16,6 @@ The reference runs the same workload as a process pool over host cores
 
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -64,7 +63,6 @@ class SplomConfig:
     iterations: int = 10
     max_batch: int = 256        # plots per batched launch (bounds the workspace: ~43 MB per plot at C4)
     collect_metrics: bool = False  # per-frame binned_stddev / overplotting of every plot ("basic")
-    streams: int = 1            # sub-batches replayed concurrently on this many streams
 
 
 class DeviceSplom:
@@ -86,15 +84,11 @@ class DeviceSplom:
         nb = len(self.ids)
         self.inputs = torch.empty((nb, n, 2), dtype=torch.float32, device=self.dev)
         self.work = torch.empty_like(self.inputs)
-        # plots of an odd size cannot share 16-byte aligned batch strides: one per launch;
-        # with several streams the block is cut into one sub-batch per stream
-        nst = max(1, min(cfg.streams, nb))
-        per = -(-nb // nst)
-        self.batch = max(1, min(cfg.max_batch, per)) if n % 2 == 0 else 1
+        # plots of an odd size cannot share 16-byte aligned batch strides: one per launch
+        self.batch = max(1, min(cfg.max_batch, nb)) if n % 2 == 0 else 1
         self.chunks = [(b0, min(b0 + self.batch, nb)) for b0 in range(0, nb, self.batch)]
-        self.streams = [torch.cuda.Stream(device=self.dev) for _ in range(min(nst, len(self.chunks)))]
         wsb = int(self.lib.inim_workspace_bytes(cfg.k, n, self.batch))
-        self.ws = [torch.empty(wsb, dtype=torch.uint8, device=self.dev) for _ in self.streams]
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
         self.stats = (torch.zeros((nb, cfg.iterations, 3), dtype=torch.int64, device=self.dev)
                       if cfg.collect_metrics else None)
 
@@ -105,28 +99,14 @@ class DeviceSplom:
     def run(self):
         """All plots, `iterations` each, on the current stream; inputs stay untouched
         (results in .work)."""
-        torch, D, lib, cfg = self.torch, self.D, self.lib, self.cfg
+        D, lib, cfg = self.D, self.lib, self.cfg
         self.work.copy_(self.inputs)
-        cur = torch.cuda.current_stream(self.dev)
-        if len(self.streams) == 1:
-            runs = [(cur, self.ws[0], c) for c in self.chunks]
-        else:  # sub-batch q on stream q % S, each stream with its own workspace
-            start = torch.cuda.Event()
-            start.record(cur)
-            for st in self.streams:
-                st.wait_event(start)
-            runs = [(self.streams[q % len(self.streams)], self.ws[q % len(self.streams)], c)
-                    for q, c in enumerate(self.chunks)]
-        for st, ws, (b0, b1) in runs:
+        stream = D.stream()
+        for b0, b1 in self.chunks:
             stats = D.ptr(self.stats[b0:b1]) if self.stats is not None else None
             self._lib.check(lib.inim_run_batched(D.ptr(self.work[b0:b1]), cfg.points, b1 - b0, cfg.k,
-                                                 cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(ws),
-                                                 ctypes.c_void_p(st.cuda_stream)), "splom run")
-        if len(self.streams) > 1:
-            for st in self.streams:
-                ev = torch.cuda.Event()
-                ev.record(st)
-                cur.wait_event(ev)
+                                                 cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(self.ws),
+                                                 stream), "splom run")
         return self.work
 
     def metrics(self):
