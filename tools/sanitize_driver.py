@@ -36,6 +36,14 @@ def main():
     r.frame(3)
     d = rng.random((4096, 4096)) * 3  # the TMA-ring reduce and the 32 x 128 tile geometry
     P.build_integral_set(d)
+    P.build_density(pts, P.RegularizationParams(k=7, kernel_size=20))  # runtime-tap smoothing
+    P.gaussian_smooth(rng.random((16, 16)), 12)                         # taps folded onto one period
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
+    cfg = SplomConfig(nplots=3, points=70_000, k=8, kernel_size=8, iterations=3, collect_metrics=True)
+    job = DeviceSplom(cfg, range(3))  # the batched run (plot index in grid.z), sorted path
+    job.load(lambda i: splom_plot(i, cfg.points))
+    job.run()
+    job.metrics()
     torch.cuda.synchronize()
     print("sanitize driver ok")
 
