@@ -3,7 +3,6 @@
 // CTA-wide barriers, so every thread of the CTA must call it.
 #pragma once
 
-#include <cooperative_groups.h>
 #include <type_traits>
 
 #include "inim_taps.cuh"
@@ -369,183 +368,6 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
         }
     }
     __syncthreads();
-}
-
-// ----------------------------------------------- cluster-fused smoothing (h + v + reduce)
-// One CTA = one VR x TW tile of d (TW = the integral tile width 32 CPL, VR = 64 rows);
-// the CTAs of a tile column form clusters of CY (<= 8) vertically adjacent tiles.
-//   1. horizontal pass of the tile's own VR rows straight from the counts into the
-//      tile buffer hs ((VR + 2R) x TWP, own rows at [R, R + VR)): 32-row chunks of the
-//      input are staged in shared memory (the next chunk's loads in flight in registers
-//      while the current one is filtered), lane = row of the chunk, warp = a TW / 8
-//      column chunk.  A CTA at a cluster edge that is not a grid edge also filters its
-//      R outer halo rows (nobody in its cluster has them).
-//   2. cluster barrier; the halo rows come from the neighbouring CTAs' hs through
-//      distributed shared memory (or, at the grid's top and bottom, from the tile's own
-//      rows by the half-sample reflection); cluster barrier (every remote read is done
-//      before the buffers are overwritten).
-//   3. vertical pass in place (fir_cols4_inplace), the tile reduce of every band from
-//      shared memory, the d store.
-// Against the two-kernel path this drops the horizontal scratch (4 B/px written, ~7 B/px
-// re-read) and one launch, and recomputes only the cluster-edge halos (2R of every
-// CY x VR rows).
-constexpr int kCRows = 64;   // VR
-constexpr int kCChunk = 32;  // staged input rows per chunk (one per lane)
-constexpr int kCThreads = 256;
-
-__host__ __device__ inline int cl_pitch(int TW, int R) {  // staging pitch: >= TW + 2R + 3, pitch / 4 odd
-    int p = (TW + 2 * R + 3 + 3) & ~3;
-    if (((p >> 2) & 1) == 0) p += 4;
-    return p;
-}
-
-__host__ __device__ inline size_t cl_smem_bytes(int TW, int R) {
-    return ((size_t)(kCRows + 2 * R) * (TW + 4) + (size_t)kCChunk * cl_pitch(TW, R)) * sizeof(float);
-}
-
-template <int R, int CPL>
-__device__ __forceinline__ void smooth_cluster_tile(const uint32_t* __restrict__ in, float* __restrict__ d,
-                                                    uint32_t* __restrict__ zero_next, const Geo& g, const Ws& ws,
-                                                    float background, int emit, int bx, int by, int cy, int CY,
-                                                    float* sm) {
-    namespace cg = cooperative_groups;
-    constexpr int TW = 32 * CPL, TWP = TW + 4, CW = TW / 8, CR = kCChunk, VR = kCRows, NTH = kCThreads;
-    static_assert(R <= VR, "halo rows come from one neighbouring tile");
-    constexpr bool VEC = (R & 3) == 0;                  // (i0 - R) is a multiple of 4: 16-byte staging loads
-    constexpr int W4 = (TW + 2 * R + 3) / 4;            // 16-byte groups per staged row
-    constexpr int PF = (CR * W4 + NTH - 1) / NTH;       // prefetch slots per thread
-    const int s = g.s, TH = g.TH;
-    const int a0 = by * VR, i0 = bx * TW;
-    const int ld = cl_pitch(TW, R);
-    float* hs = sm;                                    // [VR + 2R][TWP]
-    float* st = sm + (size_t)(VR + 2 * R) * TWP;       // [CR][ld]
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const bool vec = VEC && i0 - R >= 0 && i0 + TW + R <= s;
-    const bool top = a0 == 0, bottom = a0 + VR == s;
-    const bool haloT = !top && cy == 0, haloB = !bottom && cy == CY - 1;  // filtered here (cluster edge)
-    const int h0 = haloT ? 0 : R, h1 = haloB ? VR + 2 * R : VR + R;      // hs rows of the horizontal pass
-    const int nch = (h1 - h0 + CR - 1) / CR;
-    if (zero_next) {  // this tile's VR x TW block of the next count buffer
-        constexpr int TW4 = TW / 4;
-        for (int q = tid; q < VR * TW4; q += NTH) {
-            const int r = q / TW4, c4 = q - r * TW4;
-            reinterpret_cast<uint4*>(zero_next + (int64_t)(a0 + r) * s + i0)[c4] = make_uint4(0u, 0u, 0u, 0u);
-        }
-    }
-    // ---- 1. horizontal pass of hs rows [h0, h1), chunk by chunk
-    uint4 pf[PF];
-    auto issue = [&](int c) {
-#pragma unroll
-        for (int j = 0; j < PF; ++j) {
-            const int q = tid + j * NTH;
-            const int rr = q / W4, c4 = q - rr * W4;
-            const int r = h0 + c * CR + rr;
-            if (q < CR * W4 && r < h1) {
-                const int row = reflect_index(a0 - R + r, s);
-                pf[j] = __ldg(reinterpret_cast<const uint4*>(in + (int64_t)row * s + i0 - R) + c4);
-            }
-        }
-    };
-    auto place = [&](int c) {
-        if (vec) {
-#pragma unroll
-            for (int j = 0; j < PF; ++j) {
-                const int q = tid + j * NTH;
-                const int rr = q / W4, c4 = q - rr * W4;
-                if (q < CR * W4 && h0 + c * CR + rr < h1) {
-                    const uint4 u = pf[j];
-                    *reinterpret_cast<float4*>(st + rr * ld + 4 * c4) =
-                        make_float4((float)u.x, (float)u.y, (float)u.z, (float)u.w);
-                }
-            }
-        } else {  // tiles at the left / right border: reflected columns
-            const int Wc = TW + 2 * R;
-            for (int q = tid; q < CR * Wc; q += NTH) {
-                const int rr = q / Wc, cc = q - rr * Wc;
-                const int r = h0 + c * CR + rr;
-                if (r < h1) {
-                    const int row = reflect_index(a0 - R + r, s);
-                    st[rr * ld + cc] = (float)__ldg(in + (int64_t)row * s + reflect_index(i0 - R + cc, s));
-                }
-            }
-        }
-    };
-    if (vec) issue(0);
-#pragma unroll 1
-    for (int c = 0; c < nch; ++c) {
-        place(c);
-        __syncthreads();
-        if (vec && c + 1 < nch) issue(c + 1);  // in flight while this chunk is filtered
-        const int r = h0 + c * CR + lane;
-        if (r < h1) {
-            const float* row = st + lane * ld + w * CW;
-            float acc[CW];
-#pragma unroll
-            for (int p = 0; p < CW; ++p) acc[p] = 0.f;
-            constexpr int NT = 2 * R + 1;
-            constexpr int NQ = CW + NT - 1;
-#pragma unroll
-            for (int q4 = 0; q4 < (NQ + 3) / 4; ++q4) {
-                const float4 v4 = *reinterpret_cast<const float4*>(row + 4 * q4);
-                const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int q = 4 * q4 + e;
-#pragma unroll
-                    for (int p = 0; p < CW; ++p) {
-                        const int t = q - p;
-                        if (q < NQ && t >= 0 && t < NT) acc[p] = fmaf(TapsOf<R / 3>::w(t), vv[e], acc[p]);
-                    }
-                }
-            }
-            float4* dst = reinterpret_cast<float4*>(hs + (size_t)r * TWP + w * CW);
-#pragma unroll
-            for (int p = 0; p < CW / 4; ++p)
-                dst[p] = make_float4(acc[4 * p], acc[4 * p + 1], acc[4 * p + 2], acc[4 * p + 3]);
-        }
-        __syncthreads();  // the staging rows are refilled next
-    }
-    // ---- 2. halo rows: neighbours (distributed shared memory) or reflection
-    cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
-    {
-        constexpr int TW4 = TW / 4;
-        const float* upper = nullptr;  // hs of the tile above / below (their own rows)
-        const float* lower = nullptr;
-        if (!top && !haloT) upper = cl.map_shared_rank(hs, cl.block_rank() - 1);
-        if (!bottom && !haloB) lower = cl.map_shared_rank(hs, cl.block_rank() + 1);
-        for (int q = tid; q < R * TW4; q += NTH) {
-            const int r = q / TW4, c4 = q - r * TW4;
-            // top halo row r (global row a0 - R + r): the upper tile's own row VR - R + r,
-            // or by reflection (row -(R - r) -> R - r - 1) this tile's own row R - r - 1
-            if (!haloT) {
-                const float* src = upper ? upper + (size_t)(VR + r) * TWP : hs + (size_t)(R + R - r - 1) * TWP;
-                reinterpret_cast<float4*>(hs + (size_t)r * TWP)[c4] = reinterpret_cast<const float4*>(src)[c4];
-            }
-            // bottom halo row R + VR + r (global row a0 + VR + r): the lower tile's own row r,
-            // or by reflection (row s + r -> s - 1 - r) this tile's own row VR - 1 - r
-            if (!haloB) {
-                const float* src = lower ? lower + (size_t)(R + r) * TWP : hs + (size_t)(R + VR - 1 - r) * TWP;
-                reinterpret_cast<float4*>(hs + (size_t)(R + VR + r) * TWP)[c4] = reinterpret_cast<const float4*>(src)[c4];
-            }
-        }
-    }
-    cl.sync();  // every remote read done: the buffers are rewritten in place below
-    // ---- 3. vertical pass in place: thread = (band group, column quad), P = TH / 4 rows
-    const int grp = tid / TW, t = tid - grp * TW;
-    const int VB = VR / TH;
-    if (TH == 32) fir_cols4_inplace<R, 8>(hs, TW, grp * TH, t, grp < VB, background, TWP);
-    else fir_cols4_inplace<R, 4>(hs, TW, grp * TH, t, grp < VB, background, TWP);
-    __syncthreads();
-    if (emit) {  // the tile reduce of every band, straight from shared memory
-        for (int gb = w; gb < VB; gb += NTH / 32)
-            warp_tile_reduce<CPL>(hs + (size_t)gb * TH * TWP, TWP, g, ws, a0 / TH + gb, bx, lane);
-    }
-    constexpr int TW4 = TW / 4;
-    for (int q = tid; q < VR * TW4; q += NTH) {
-        const int r = q / TW4, c4 = q - r * TW4;
-        reinterpret_cast<float4*>(d + (int64_t)(a0 + r) * s + i0)[c4] = *reinterpret_cast<const float4*>(hs + r * TWP + 4 * c4);
-    }
 }
 
 }  // namespace inim

@@ -38,55 +38,6 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
                      blockIdx.y, vsm);
 }
 
-// The iteration's smoothing of the counts in one launch: horizontal + vertical pass +
-// tile reduce, vertical halos exchanged through distributed shared memory within
-// clusters of vertically adjacent tiles (inim_smooth.cuh smooth_cluster_tile).
-template <int R, int CPL>
-__global__ void __launch_bounds__(kCThreads) smooth_cluster_kernel(const uint32_t* __restrict__ in,
-                                                                   float* __restrict__ d,
-                                                                   uint32_t* __restrict__ zero_next, const Geo g,
-                                                                   const Ws ws, float background, int emit,
-                                                                   const int* state, int64_t zslab) {
-    pdl_enter();
-    if (state && state[0]) return;  // uniform over the grid: no CTA waits at a cluster barrier alone
-    extern __shared__ __align__(16) float csm[];
-    const int64_t zo = zslab_off(zslab);  // plot blockIdx.z of a batch
-    const cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-    smooth_cluster_tile<R, CPL>(zoff(in, zo), zoff(d, zo), zoff_opt(zero_next, zo), g, ws_shift(ws, zo), background,
-                                emit, blockIdx.x, blockIdx.y, (int)cl.block_rank(), (int)cl.num_blocks(), csm);
-}
-
-constexpr int kMaxClusterRows = 8;  // portable cluster size
-
-template <int R, int CPL>
-inline int launch_cluster(const uint32_t* counts, float* d, uint32_t* zero_next, const Geo& g, const Ws& ws, float bg,
-                          int emit, const int* state, cudaStream_t st, const Bat& bt) {
-    const size_t smem = cl_smem_bytes(g.TW, R);
-    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_cluster_kernel<R, CPL>, (int)smem));
-    const int ty = g.s / kCRows;
-    const int cy = ty < kMaxClusterRows ? ty : kMaxClusterRows;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(g.NX, ty, bt.B);
-    cfg.blockDim = dim3(kCThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = cy;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    INIM_CUDA_TRY(cudaLaunchKernelEx(&cfg, smooth_cluster_kernel<R, CPL>, counts, d, zero_next, g, ws, bg, emit, state,
-                                     bt.slab));
-    prof_mark(st, emit ? "smooth_cluster_reduce" : "smooth_cluster");
-    return (int)cudaGetLastError();
-}
-
-bool cluster_smooth_enabled();  // smooth.cu (INIM_CLUSTER_SMOOTH=0 selects the two-kernel path)
-
 template <int R, typename T>
 inline int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, uint32_t* zero_next,
                     cudaStream_t st, const Bat& bt) {
@@ -118,12 +69,6 @@ template <int KS>
 int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt) {
     constexpr int R = 3 * KS;
-    // the counts of the iteration on grids of 64^2 and up: one cluster launch
-    if (counts && g.s >= kCRows && cluster_smooth_enabled()) {
-        const uint32_t* c = static_cast<const uint32_t*>(in);
-        if (g.CPL == 4) return launch_cluster<R, 4>(c, d, zero_next, g, ws, bg, emit, state, st, bt);
-        if (g.CPL == 2) return launch_cluster<R, 2>(c, d, zero_next, g, ws, bg, emit, state, st, bt);
-    }
     int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st,
                                             bt)
                     : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st, bt);

@@ -11,18 +11,6 @@
 
 namespace inim {
 
-// INIM_CLUSTER_SMOOTH=0: the two-kernel smoothing (horizontal pass through the workspace
-// scratch, then vertical pass + reduce) instead of the cluster-fused kernel (A/B and the
-// equivalence test).
-bool cluster_smooth_enabled() {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = getenv("INIM_CLUSTER_SMOOTH");
-        env = (e && e[0] == '0') ? 0 : 1;
-    }
-    return env == 1;
-}
-
 // ------------------------------------------------------- generic taps (kernel_size > 16)
 // The compiled FIRs carry the taps of kernel_size 1..16 as FFMA immediates.  Any
 // larger kernel (the reference accepts every kernel_size >= 1, density.py:40-51) runs

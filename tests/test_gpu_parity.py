@@ -463,44 +463,3 @@ def test_field_layouts_bit_identical(tmp_path, k):
         assert out.returncode == 0, out.stderr[-2000:]
         outs.append(np.load(dst))
     assert np.array_equal(outs[0], outs[1])
-
-
-@pytest.mark.parametrize("k,ks", [(6, 8), (7, 16), (10, 8), (12, 8), (9, 3), (11, 5)])
-def test_cluster_smoothing_bit_identical_to_two_pass(tmp_path, k, ks):
-    """The cluster-fused smoothing (horizontal + vertical + tile reduce in one launch,
-    vertical halos exchanged through distributed shared memory; the default) and the
-    two-kernel path through the workspace scratch (INIM_CLUSTER_SMOOTH=0) give
-    bit-identical runs: same taps, same per-output accumulation order."""
-    import os
-    import subprocess
-    import sys
-    import textwrap
-
-    from conftest import ROOT
-
-    host = clusters(90_000, k).astype(np.float32)
-    np.save(tmp_path / "in.npy", host)
-    outs = []
-    for mode in ("0", "1"):
-        dst = tmp_path / f"out{mode}.npy"
-        script = textwrap.dedent(f"""
-            import sys
-            sys.path.insert(0, {str(ROOT)!r})
-            import numpy as np, torch
-            from paper_2408_06513_b200 import _device as D, _lib
-            lib = _lib.load()
-            host = np.load({str(tmp_path / "in.npy")!r})
-            n = len(host)
-            ws = torch.empty(int(lib.inim_workspace_bytes({k}, n, 1)), dtype=torch.uint8, device="cuda")
-            a = torch.from_numpy(host).cuda()
-            _lib.check(lib.inim_run_uncached(D.ptr(a), n, {k}, {ks}, 0.0, 3, 0.0, None, None, None, None, None,
-                                             D.ptr(ws), D.stream()), "run")
-            np.save({str(dst)!r}, a.cpu().numpy())
-        """)
-        f = tmp_path / f"cl{mode}.py"
-        f.write_text(script)
-        out = subprocess.run([sys.executable, str(f)], capture_output=True, text=True, timeout=300,
-                             env=dict(os.environ, INIM_CLUSTER_SMOOTH=mode))
-        assert out.returncode == 0, out.stderr[-2000:]
-        outs.append(np.load(dst))
-    assert np.array_equal(outs[0], outs[1])
