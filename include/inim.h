@@ -196,8 +196,10 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
  * pts: device (B, n, 2) float32, updated in place to each plot's final positions (n
  * even when B > 1); ws: inim_workspace_bytes(k, n, B) bytes.  frame_stats: NULL, or
  * device u64[B][iterations][3] (cleared by the call) receiving the per-frame occupancy
- * statistics of every plot (as inim_run_metrics; collect_metrics="basic").  The result
- * of each plot is bit-identical to inim_run on that plot alone. */
+ * statistics of every plot (as inim_run_metrics; collect_metrics="basic").  Batches
+ * use the wide tile geometry (32 x 128 tiles from 128^2 up; a single plot uses 16 x 64
+ * up to 2048^2), so each plot matches inim_run on that plot alone within float32
+ * rounding (the tile sums associate differently), and a replay is bit-identical. */
 int inim_run_batched(float* pts, int64_t n, int B, int k, int kernel_size, float background, int iterations,
                      unsigned long long* frame_stats, void* ws, cudaStream_t stream);
 

@@ -205,10 +205,10 @@ static std::vector<RunEntry> g_cache;
 // excursions / state / neighbourhood metrics are not recorded: fixed iterations only).
 static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fields, float* disp, float* excursions,
                        int* state, void* ws, cudaStream_t st) {
-    const Geo g = make_geo(key.k);
+    const int B = key.B > 1 ? key.B : 1;
+    const Geo g = make_geo(key.k, B > 1);  // batches: the wide tile geometry
     const FullLayout F = full_layout(g, key.n);
     const Ws w = make_ws(ws, F.L);
-    const int B = key.B > 1 ? key.B : 1;
     // plot strides: workspace slabs (bytes) and the caller's (B, n, 2) points (floats)
     const Bat bt{B, B > 1 ? (int64_t)F.bytes : 0, B > 1 ? 2 * key.n : 0};
     const int64_t zs = bt.slab / (int64_t)sizeof(float);  // slab stride in floats (workspace point buffers)
@@ -336,7 +336,7 @@ const char* inim_version(void) { return "libinim sm_100a 0.1"; }
 
 size_t inim_workspace_bytes(int k, int64_t n, int B) {
     if (!k_ok(k) || n < 0) return 0;
-    return full_layout(make_geo(k), n).bytes * (size_t)(B > 1 ? B : 1);
+    return full_layout(make_geo(k, B > 1), n).bytes * (size_t)(B > 1 ? B : 1);
 }
 
 int inim_splat(const void* pts, int pts_is_f64, int64_t n, int k, uint32_t* counts, cudaStream_t stream) {

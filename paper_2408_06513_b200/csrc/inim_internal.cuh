@@ -41,16 +41,19 @@ struct Geo {
 };
 
 // Bands of 16 rows up to 2048^2 (more CTAs for latency-bound small grids), 32 rows
-// above (fewer carry vectors per pixel for bandwidth-bound large grids).
-inline Geo make_geo(int k) {
+// above (fewer carry vectors per pixel for bandwidth-bound large grids).  `wide`: the
+// large-grid geometry from 128^2 up, for plot batches (thousands of tiles in flight
+// anyway: the per-tile prologue is amortised over 4x the pixels).
+inline Geo make_geo(int k, bool wide = false) {
     Geo g;
     g.k = k;
     g.s = 1 << k;
     g.m = (int64_t)g.s * g.s;
-    g.TH = g.s < 16 ? g.s : (g.s <= 2048 ? 16 : 32);
+    const bool large = g.s > 2048 || (wide && g.s >= 128);
+    g.TH = g.s < 16 ? g.s : (large ? 32 : 16);
     // one warp per tile: 64 columns (2 per lane) up to 2048^2 for more warps on small
     // grids, 128 columns (4 per lane, 16-byte accesses) above
-    g.TW = g.s <= 2048 ? (g.s < 64 ? g.s : 64) : 128;
+    g.TW = large ? 128 : (g.s < 64 ? g.s : 64);
     g.CPL = g.TW >= 128 ? 4 : (g.TW >= 64 ? 2 : 1);
     g.B = g.s / g.TH;
     g.NX = g.s / g.TW;
