@@ -7,6 +7,10 @@
 
 #include "inim_points.cuh"
 
+#ifndef INIM_BATCH_MOVE_U
+#define INIM_BATCH_MOVE_U 4
+#endif
+
 namespace inim {
 
 // Warp-aggregated integer atomics: lanes hitting the same pixel in one step are
@@ -497,9 +501,12 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
     const int64_t npair = n >> 1;
     // two point pairs (two 16-byte loads) per thread per step (measured: 1 or 4 are
     // slower at C2)
-    auto kern = bt.B > 1 ? (pairs ? sample_f32_kernel<true, 2, true> : sample_f32_kernel<false, 2, true>)
+    // a batch (HBM-latency bound, work for many waves): UB point pairs per thread
+    constexpr int UB = INIM_BATCH_MOVE_U;
+    auto kern = bt.B > 1 ? (pairs ? sample_f32_kernel<true, UB, true> : sample_f32_kernel<false, UB, true>)
                          : (pairs ? sample_f32_kernel<true, 2, false> : sample_f32_kernel<false, 2, false>);
-    const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair, 256 * 2, bt);
+    const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair,
+                                 256 * (bt.B > 1 ? UB : 2), bt);
     INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, reinterpret_cast<const float4*>(in), in,
                              reinterpret_cast<float4*>(out), out, n, clip, max_disp, state, splat_next, zn0, zn1,
                              sorted ? 1 : 0, zin, zout, bt.slab));
