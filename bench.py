@@ -98,7 +98,7 @@ def measured_peaks() -> dict:
 class ClockSampler(threading.Thread):
     """Samples SM clock and throttle reasons through NVML during the timed region."""
 
-    def __init__(self, index: int, period: float = 0.005):
+    def __init__(self, index: int, period: float = 0.001):
         super().__init__(daemon=True)
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
@@ -504,30 +504,38 @@ def bench_reference(args, workload: str):
 
 
 class _StubSplom:
-    """CPU stand-in for DeviceSplom (--cpu-stub): the same shard / run / gather plumbing
-    with the per-plot compute replaced by a deterministic transform, so the multi-rank
-    path of this file runs on gloo without a GPU (tests/test_distributed.py)."""
+    """CPU stand-in for DeviceSplom (--cpu-stub): the same shard / chunked run /
+    pipelined gather plumbing with the per-plot compute replaced by a deterministic
+    transform, so the multi-rank path of this file runs on gloo without a GPU
+    (tests/test_distributed.py)."""
 
-    def __init__(self, ids, points):
+    def __init__(self, ids, points, batch):
         import torch
 
         self.ids = list(ids)
         self.work = torch.zeros((len(self.ids), points, 2), dtype=torch.float32)
+        self.chunks = [(b0, min(b0 + batch, len(self.ids))) for b0 in range(0, len(self.ids), batch)]
 
-    def run(self):
-        for q, idx in enumerate(self.ids):
-            self.work[q].fill_(float(idx))
+    def run(self, on_chunk=None):
+        for b0, b1 in self.chunks:
+            for q in range(b0, b1):
+                self.work[q].fill_(float(self.ids[q]))
+            if on_chunk is not None:
+                on_chunk(b0, b1)
         return self.work
 
 
 def splom_job(args, world: int, rank: int, device_stub: bool):
-    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, shard, splom_plot
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, pipeline_parts, shard, splom_plot
 
     ids = shard(args.plots, world, rank)
     points = args.splom_points
+    # with a pipelined gather the block runs as sub-batches of the pipeline's width
+    batch = pipeline_parts(args.plots, world, args.gather_parts)[0][1] if world > 1 else args.plots
     if device_stub:
-        return _StubSplom(ids, points), ids
-    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS)
+        return _StubSplom(ids, points, max(1, batch)), ids
+    cfg = SplomConfig(nplots=args.plots, points=points, k=K_GRID, kernel_size=KERNEL_SIZE, iterations=ITERS,
+                      max_batch=max(1, batch))
     job = DeviceSplom(cfg, ids)
     job.load(lambda i: splom_plot(i, points))
     return job, ids
@@ -546,15 +554,21 @@ def bench_splom(args, emit: bool = True):
     if not stub:
         torch.cuda.set_device(local)
     dist = init_dist(world, "gloo" if stub else "nccl")
-    from paper_2408_06513_b200.splom import gather_results
+    from paper_2408_06513_b200.splom import GatherPipeline
 
     job, ids = splom_job(args, world, rank, stub)
     flush = None if stub else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     gathered = {}
 
     def step():
-        res = job.run()
-        gathered["all"] = gather_results(res, args.plots, world) if world > 1 else res
+        if world == 1:
+            gathered["all"] = job.run()
+            return
+        # each sub-batch's all-gather starts as soon as its batched run is enqueued and
+        # overlaps the next sub-batch's compute
+        pipe = GatherPipeline(args.plots, world, rank, args.gather_parts, job.work)
+        job.run(on_chunk=lambda b0, b1: pipe.ready(job.work, b1))
+        gathered["all"] = pipe.finish(job.work)
 
     def sync():
         if not stub:
@@ -617,7 +631,8 @@ def bench_splom(args, emit: bool = True):
                      "algorithmic_bytes_per_plot_iteration": SPLOM_BYTES_PER_PLOT_ITER,
                      "method": "24 n + 24 m bytes per plot-iteration (SURVEY 8(d)) x plot-iterations / s"},
         "collective": {"backend": dist.get_backend() if world > 1 else None, "world": world,
-                       "op": "all_gather_into_tensor of final positions" if world > 1 else None,
+                       "op": (f"all_gather_into_tensor of final positions in {args.gather_parts} sub-batches, each "
+                              "overlapping the next sub-batch's compute") if world > 1 else None,
                        "bytes_per_step": int(args.plots * args.splom_points * 8) if world > 1 else 0,
                        "gather_ok": gather_ok},
         "plots_per_rank": len(ids),
@@ -731,6 +746,7 @@ def main():
                          "c3: 16M pts/4096^2; sweep: integral-only 512^2..16384^2")
     ap.add_argument("--plots", type=int, default=256)
     ap.add_argument("--splom-points", type=int, default=SPLOM_POINTS)
+    ap.add_argument("--gather-parts", type=int, default=2, help="N > 1: sub-batches of the pipelined gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-splom", action="store_true", help="N = 1: leave the SPLOM batch out of the C2 line")
     ap.add_argument("--cpu-stub", action="store_true", help="multi-rank plumbing on gloo, no GPU (tests)")

@@ -96,9 +96,10 @@ class DeviceSplom:
         for q, idx in enumerate(self.ids):
             self.inputs[q].copy_(self.torch.from_numpy(make_plot(idx).astype(np.float32)))
 
-    def run(self):
+    def run(self, on_chunk: Optional[Callable[[int, int], None]] = None):
         """All plots, `iterations` each, on the current stream; inputs stay untouched
-        (results in .work)."""
+        (results in .work).  on_chunk(b0, b1) is called after each batched run of plots
+        [b0, b1) is enqueued (a pipelined gather starts that chunk's collective there)."""
         D, lib, cfg = self.D, self.lib, self.cfg
         self.work.copy_(self.inputs)
         stream = D.stream()
@@ -107,6 +108,8 @@ class DeviceSplom:
             self._lib.check(lib.inim_run_batched(D.ptr(self.work[b0:b1]), cfg.points, b1 - b0, cfg.k,
                                                  cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(self.ws),
                                                  stream), "splom run")
+            if on_chunk is not None:
+                on_chunk(b0, b1)
         return self.work
 
     def metrics(self):
@@ -147,10 +150,92 @@ def gather_results(local, nplots: int, world: int, group=None):
     return torch.cat(parts, dim=0)
 
 
-def run_distributed(cfg: SplomConfig, rank: int, world: int, make_plot: Optional[Callable] = None, group=None):
-    """One rank's share of the batch + the gather; returns all final positions."""
+def pipeline_parts(nplots: int, world: int, parts: int) -> list:
+    """Offsets [b0, b1) within every rank's block of the pipelined gather's sub-batches
+    (the same on every rank: blocks are padded to the largest shard)."""
+    per = max(len(shard(nplots, world, r)) for r in range(world))
+    step = max(1, -(-per // max(1, parts)))
+    return [(b0, min(b0 + step, per)) for b0 in range(0, per, step)]
+
+
+class GatherPipeline:
+    """The gather of the final positions split into sub-batches, each started as soon as
+    its batched run is enqueued (asynchronous collective: NCCL runs it on its own stream
+    after the compute stream reaches that point), so the transfer of sub-batch q
+    overlaps the compute of sub-batch q + 1.  finish() waits and reassembles the plots in
+    global order (rank blocks, padding dropped)."""
+
+    def __init__(self, nplots: int, world: int, rank: int, parts: int, like, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.nplots, self.world, self.rank = nplots, world, rank
+        self.bounds = pipeline_parts(nplots, world, parts)
+        self.nccl = world > 1 and dist.get_backend(group) == "nccl"
+        self.shape = tuple(like.shape[1:])
+        self.dtype, self.device = like.dtype, like.device
+        self.counts = [len(shard(nplots, world, r)) for r in range(world)]
+        self.works, self.outs = [], []
+
+    def ready(self, local, b1: int):
+        """This rank's plots [0, b1) of its block (`local`) are computed (enqueued): start
+        every sub-batch collective they complete, in order (the same order on every
+        rank; a short block completes its later sub-batches at once)."""
+        n = local.shape[0]
+        while len(self.outs) < len(self.bounds):
+            c0, c1 = self.bounds[len(self.outs)]
+            if min(c1, n) > b1:
+                break
+            self._submit(local, len(self.outs))
+
+    def _submit(self, local, q: int):
+        torch, dist = self.torch, self.dist
+        c0, c1 = self.bounds[q]
+        width = c1 - c0
+        have = max(0, min(local.shape[0], c1) - c0)
+        if have == width:
+            src = local[c0:c1]
+        else:  # a short (or empty) last block: pad to the common width
+            src = torch.zeros((width,) + self.shape, dtype=self.dtype, device=self.device)
+            if have:
+                src[:have].copy_(local[c0:c0 + have])
+        if self.world == 1:
+            self.outs.append([src])
+            return
+        if self.nccl:
+            out = torch.empty((self.world, width) + self.shape, dtype=self.dtype, device=self.device)
+            self.works.append(dist.all_gather_into_tensor(out, src.contiguous(), group=self.group, async_op=True))
+            self.outs.append([out[r] for r in range(self.world)])
+        else:  # gloo (CPU tests): list form
+            blocks = [torch.empty_like(src) for _ in range(self.world)]
+            self.works.append(dist.all_gather(blocks, src.contiguous(), group=self.group, async_op=True))
+            self.outs.append(blocks)
+
+    def finish(self, local):
+        self.ready(local, local.shape[0])
+        for w in self.works:
+            w.wait()
+        parts = []
+        for r in range(self.world):
+            for q, (c0, c1) in enumerate(self.bounds):
+                n = max(0, min(self.counts[r], c1) - c0)
+                if n:
+                    parts.append(self.outs[q][r][:n])
+        self.works, self.outs = [], []
+        return self.torch.cat(parts, dim=0)
+
+
+def run_distributed(cfg: SplomConfig, rank: int, world: int, make_plot: Optional[Callable] = None, group=None,
+                    gather_parts: int = 1):
+    """One rank's share of the batch + the gather; returns all final positions.  With
+    gather_parts > 1 the rank's block runs as that many sub-batches, each gathered while
+    the next one computes."""
     ids = shard(cfg.nplots, world, rank)
+    if gather_parts > 1:
+        cfg = SplomConfig(**{**cfg.__dict__, "max_batch": pipeline_parts(cfg.nplots, world, gather_parts)[0][1]})
     job = DeviceSplom(cfg, ids)
     job.load(make_plot or (lambda i: splom_plot(i, cfg.points)))
-    res = job.run()
-    return gather_results(res, cfg.nplots, world, group)
+    pipe = GatherPipeline(cfg.nplots, world, rank, gather_parts, job.work, group)
+    job.run(on_chunk=lambda b0, b1: pipe.ready(job.work, b1))
+    return pipe.finish(job.work)

@@ -140,3 +140,43 @@ def test_bench_rejects_mismatched_world():
     out = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--cpu-stub"],
                          capture_output=True, text=True, timeout=300, env=env, cwd=str(root))
     assert out.returncode != 0 and "WORLD_SIZE=1" in out.stderr
+
+
+def _pipe_worker(rank, world, port, nplots, parts, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2408_06513_b200.splom import GatherPipeline, pipeline_parts, shard
+
+        ids = list(shard(nplots, world, rank))
+        local = torch.stack([torch.full((3, 2), float(i)) for i in ids]) if ids else torch.zeros((0, 3, 2))
+        pipe = GatherPipeline(nplots, world, rank, parts, torch.zeros((1, 3, 2)))
+        step = pipeline_parts(nplots, world, parts)[0][1]
+        for b0 in range(0, len(ids), step):  # the chunked run's callbacks
+            pipe.ready(local, min(b0 + step, len(ids)))
+        allres = pipe.finish(local)
+        out_q.put((rank, allres[:, 0, 0].tolist()))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:
+        out_q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("nplots,parts", [(7, 2), (8, 3), (3, 2), (9, 4), (8, 1)])
+def test_pipelined_gather_world2(nplots, parts):
+    """Sub-batched gather: every rank submits the same collectives in the same order
+    (short blocks pad, empty sub-batches included) and the plots come back in global
+    order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_worker, args=(r, 2, port, nplots, parts, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        assert res[r] == [float(i) for i in range(nplots)], res[r]
