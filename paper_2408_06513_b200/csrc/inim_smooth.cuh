@@ -6,6 +6,10 @@
 #include <type_traits>
 
 #include "inim_taps.cuh"
+
+#ifndef INIM_FFMA2_V
+#define INIM_FFMA2_V 1  // vertical pass on packed fma.rn.f32x2 (0: scalar FFMA immediates)
+#endif
 #include "inim_tiles.cuh"
 
 namespace inim {
@@ -243,6 +247,37 @@ __device__ __forceinline__ void fir_cols4_inplace(float* __restrict__ sh, int TW
 #pragma unroll
     for (int pp = 0; pp < P; ++pp) acc[pp] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live) {
+#if INIM_FFMA2_V
+        // packed FP32: the column pairs (x, y) and (z, w) of the quad share each tap, so
+        // one fma.rn.f32x2 (FFMA2) does two of the FMAs; the tap pairs come from constant
+        // memory and stay in uniform registers.  Each lane's arithmetic is the same
+        // fma.rn as the scalar form, in the same order: bit-identical results, half the
+        // FMA instructions (issue slots for the loads and address math).
+        uint64_t a2[P][2];
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) a2[pp][0] = a2[pp][1] = 0ull;
+#pragma unroll
+        for (int q = 0; q < P + NT - 1; ++q) {
+            const float4 v4 = *reinterpret_cast<const float4*>(sh + (r0 + q) * ld + 4 * quad);
+            uint64_t lo, hi;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(lo) : "f"(v4.x), "f"(v4.y));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(hi) : "f"(v4.z), "f"(v4.w));
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) {
+                const int tp = q - pp;
+                if (tp >= 0 && tp < NT) {
+                    const uint64_t w2 = TapsOf<R / 3>::pair(tp);
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a2[pp][0]) : "l"(w2), "l"(lo));
+                    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a2[pp][1]) : "l"(w2), "l"(hi));
+                }
+            }
+        }
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) {
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[pp].x), "=f"(acc[pp].y) : "l"(a2[pp][0]));
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[pp].z), "=f"(acc[pp].w) : "l"(a2[pp][1]));
+        }
+#else
 #pragma unroll
         for (int q = 0; q < P + NT - 1; ++q) {
             const float4 v4 = *reinterpret_cast<const float4*>(sh + (r0 + q) * ld + 4 * quad);
@@ -258,6 +293,7 @@ __device__ __forceinline__ void fir_cols4_inplace(float* __restrict__ sh, int TW
                 }
             }
         }
+#endif
     }
     __syncthreads();  // every input row has been read
     if (live) {

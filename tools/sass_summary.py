@@ -12,7 +12,7 @@ from collections import Counter, defaultdict
 from pathlib import Path
 
 LIB = Path(sys.argv[1]) if len(sys.argv) > 1 else Path(__file__).resolve().parent.parent / "paper_2408_06513_b200" / "libinim.so"
-KEYS = ["UTMALDG", "UBLKCP", "SYNCS", "MATCH", "REDG", "RED", "ATOMG", "ATOM", "FFMA", "DFMA", "DADD", "LDG", "STG",
+KEYS = ["UTMALDG", "UBLKCP", "SYNCS", "MATCH", "REDG", "RED", "ATOMG", "ATOM", "FFMA2", "FFMA", "DFMA", "DADD", "LDG", "STG",
         "LDS", "STS", "SHFL", "BAR", "FMNMX"]
 
 
