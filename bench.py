@@ -653,9 +653,10 @@ def job_launches(job) -> int:
 
 
 def splom_e2e(args, job, world, dist):
-    """The same step through the public API with host buffers: every rank copies its
-    block of plots from pinned host memory (float32, as the batch API takes them),
-    runs it, and copies its block of final positions back; time = max over ranks."""
+    """The same step through the public API with host buffers: every rank runs its
+    block of plots from page-locked host memory (float32, as the batch API takes them)
+    with DeviceSplom.run_host, whose chunked copies in and out overlap the batched runs,
+    and holds its block of final positions on the host; time = max over ranks."""
     import torch
 
     host_in = torch.empty(tuple(job.inputs.shape), dtype=torch.float32).pin_memory()
@@ -663,9 +664,7 @@ def splom_e2e(args, job, world, dist):
     host_out = torch.empty_like(host_in).pin_memory()
 
     def call():
-        job.inputs.copy_(host_in, non_blocking=True)
-        res = job.run()
-        host_out.copy_(res, non_blocking=True)
+        job.run_host(host_in, host_out)
         torch.cuda.current_stream().synchronize()
 
     for _ in range(2):
@@ -685,32 +684,8 @@ def splom_e2e(args, job, world, dist):
     nbytes = int(host_in.numel() * 4)
     return {"value": args.plots * ITERS / dt, "unit": "plot-iters/s", "h2d_bytes_per_step": nbytes,
             "d2h_bytes_per_step": nbytes, "ms_per_call": dt * 1e3, "statistic": "median wall time, max over ranks",
-            "api": "DeviceSplom.run (inim_run_batched) with pinned float32 host buffers, each rank its own block"}
-
-
-def bench_sweep(args):
-    """BASELINE configs[4]: integral-image-only sweep 512^2 .. 16384^2, fp32, L2 flushed."""
-    import torch
-
-    from paper_2408_06513_b200 import _device as D
-    from paper_2408_06513_b200 import _lib
-
-    lib = _lib.load()
-    dev = torch.device("cuda", 0)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    sampler = ClockSampler(0)
-    sampler.start()
-    rows = bench_integral(lib, D, dev, flush, sizes=tuple(range(9, 15)), reps=max(5, args.steps))
-    clocks = sampler.summary()
-    best = max(rows, key=lambda r: r["frac"])
-    line = {"metric": "integral-image GB/s vs HBM peak (36 B/px: read d, write 8 fp32 tables)",
-            "value": best["GB_s"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": 3,
-            "ms_per_step": best["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic uniform random textures",
-            "config": {"workload": "integral-image-only sweep 512^2..16384^2 (BASELINE configs[4])",
-                       "best_size": best["size"]},
-            "sweep": rows, "clocks": clocks}
-    print(json.dumps(line), flush=True)
+            "api": "DeviceSplom.run_host (chunked H2D / inim_run_batched / D2H overlapped on three streams), "
+                   "pinned float32 host buffers, each rank its own block"}
 
 
 def _free_port() -> int:

@@ -197,9 +197,10 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
  * even when B > 1); ws: inim_workspace_bytes(k, n, B) bytes.  frame_stats: NULL, or
  * device u64[B][iterations][3] (cleared by the call) receiving the per-frame occupancy
  * statistics of every plot (as inim_run_metrics; collect_metrics="basic").  Batches
- * use the wide tile geometry (32 x 128 tiles from 128^2 up; a single plot uses 16 x 64
- * up to 2048^2), so each plot matches inim_run on that plot alone within float32
- * rounding (the tile sums associate differently), and a replay is bit-identical. */
+ * (any B, one plot included) use the wide tile geometry (32 x 128 tiles from 128^2 up;
+ * inim_run uses 16 x 64 up to 2048^2), so each plot matches inim_run on that plot alone
+ * within float32 rounding (the tile sums associate differently), and a plot's result
+ * does not depend on B or on its position in the batch (bit-identical). */
 int inim_run_batched(float* pts, int64_t n, int B, int k, int kernel_size, float background, int iterations,
                      unsigned long long* frame_stats, void* ws, cudaStream_t stream);
 

@@ -3,6 +3,7 @@
 // CUDA-graph replay.
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -189,7 +190,7 @@ struct RunKey {
     const void *fstats, *orig_sub, *pick, *moved_sub, *nbstats;
     int64_t n_sub;
     int n_neighbors;
-    int B;  // plots in a batch (inim_run_batched), else 0
+    int B;  // plots of an inim_run_batched call (>= 1); 0 for inim_run
     bool operator==(const RunKey& o) const { return memcmp(this, &o, sizeof(RunKey)) == 0; }
 };
 
@@ -207,7 +208,8 @@ static std::vector<RunEntry> g_cache;
 static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fields, float* disp, float* excursions,
                        int* state, void* ws, cudaStream_t st) {
     const int B = key.B > 1 ? key.B : 1;
-    const Geo g = make_geo(key.k, B > 1);  // batches: the wide tile geometry
+    const bool batched = key.B > 0;              // inim_run_batched (any B, one plot included)
+    const Geo g = make_geo(key.k, batched);      // batches: the wide tile geometry
     const FullLayout F = full_layout(g, key.n);
     const Ws w = make_ws(ws, F.L);
     // plot strides: workspace slabs (bytes) and the caller's (B, n, 2) points (floats)
@@ -297,7 +299,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         // the move reads the paired field layout (two 16-byte gathers per point) while the
         // field stays L2-resident: one plot up to 2048^2 (INIM_PAIRS overrides); a batch's
         // fields stream through HBM, where the plain (s, s, 2) layout's half bytes win
-        const bool pairs = use_pairs(g, B);
+        const bool pairs = use_pairs(g, batched ? 2 : 1);
         float* plain = tg ? tg : (pairs ? nullptr : tg_scratch);
         int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, plain, exc_at(t),
                                    disp_at(t), key.eps, state, w, mp, st, pairs ? tg_scratch : nullptr, chain, bt,
@@ -337,7 +339,10 @@ const char* inim_version(void) { return "libinim sm_100a 0.1"; }
 
 size_t inim_workspace_bytes(int k, int64_t n, int B) {
     if (!k_ok(k) || n < 0) return 0;
-    return full_layout(make_geo(k, B > 1), n).bytes * (size_t)(B > 1 ? B : 1);
+    // a slab holds either geometry: inim_run (16 x 64 tiles up to 2048^2) and
+    // inim_run_batched (32 x 128 tiles from 128^2 up, any B) share the size
+    const size_t slab = std::max(full_layout(make_geo(k, false), n).bytes, full_layout(make_geo(k, true), n).bytes);
+    return slab * (size_t)(B > 1 ? B : 1);
 }
 
 int inim_splat(const void* pts, int pts_is_f64, int64_t n, int k, uint32_t* counts, cudaStream_t stream) {

@@ -112,6 +112,46 @@ class DeviceSplom:
                 on_chunk(b0, b1)
         return self.work
 
+    def run_host(self, host_in, host_out, chunk: int = 64):
+        """The whole block from page-locked host buffers: (B, n, 2) float32 in, final
+        positions out.  The plots go in chunks of `chunk`: chunk c + 1 is copied in on
+        one copy stream and chunk c - 1 copied out on another while chunk c runs (the
+        copy engines work beside the SMs), so the step costs about max(compute,
+        transfers) instead of their sum.  Returns host_out."""
+        torch, D, lib, cfg = self.torch, self.D, self.lib, self.cfg
+        nb = len(self.ids)
+        chunk = max(1, min(chunk, self.batch))
+        cur = torch.cuda.current_stream(self.dev)
+        h2d, d2h = torch.cuda.Stream(device=self.dev), torch.cuda.Stream(device=self.dev)
+        start = torch.cuda.Event()
+        start.record(cur)
+        h2d.wait_event(start)
+        d2h.wait_event(start)
+        copied, ran = [], []
+        bounds = [(b0, min(b0 + chunk, nb)) for b0 in range(0, nb, chunk)]
+        for b0, b1 in bounds:  # all copies in, in order, on their own stream
+            with torch.cuda.stream(h2d):
+                self.work[b0:b1].copy_(host_in[b0:b1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                copied.append(ev)
+        for (b0, b1), ev in zip(bounds, copied):
+            cur.wait_event(ev)
+            stats = D.ptr(self.stats[b0:b1]) if self.stats is not None else None
+            self._lib.check(lib.inim_run_batched(D.ptr(self.work[b0:b1]), cfg.points, b1 - b0, cfg.k,
+                                                 cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(self.ws),
+                                                 D.stream()), "splom run")
+            done = torch.cuda.Event()
+            done.record(cur)
+            ran.append(done)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(done)
+                host_out[b0:b1].copy_(self.work[b0:b1], non_blocking=True)
+        fin = torch.cuda.Event()
+        fin.record(d2h)
+        cur.wait_event(fin)
+        return host_out
+
     def metrics(self):
         """Per plot and frame 1..iterations: (binned_stddev, overplotting) as the
         reference's record_for_frame (metrics.py:46-71, 147-168), from the device

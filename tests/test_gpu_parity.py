@@ -414,6 +414,13 @@ def test_splom_batch_matches_single_plot_runs(P, oracle, points, iters, max_batc
         assert mets[i][-1] == pytest.approx(want, rel=1e-12, abs=0), i
     again = job.run().cpu().numpy().astype(np.float64)  # graph replay: same answer
     assert np.array_equal(again, res)
+    import torch  # host buffers, chunked copies overlapping the runs: the same answer
+    hin = torch.empty(tuple(job.inputs.shape), dtype=torch.float32).pin_memory()
+    hin.copy_(job.inputs.cpu())
+    hout = torch.empty_like(hin).pin_memory()
+    job.run_host(hin, hout, chunk=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(hout.numpy().astype(np.float64), res)
 
 
 @pytest.mark.parametrize("k", [11, 12])
