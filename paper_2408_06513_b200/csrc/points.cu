@@ -11,6 +11,7 @@
 #define INIM_BATCH_MOVE_U 4
 #endif
 
+
 namespace inim {
 
 // Warp-aggregated integer atomics: lanes hitting the same pixel in one step are
@@ -499,14 +500,16 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
                       const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1,
                       bool sorted, const Bat& bt, int64_t zin, int64_t zout) {
     const int64_t npair = n >> 1;
-    // two point pairs (two 16-byte loads) per thread per step (measured: 1 or 4 are
-    // slower at C2)
+    // point pairs (16-byte loads) per thread per step, measured per regime (DESIGN.md
+    // 4.5): two for one plot on the L2-resident paired field (C2: one 50.6, four 49.2
+    // vs 46.2 us per iteration), one on the plain field above 2048^2 (C3: 336.6 vs
+    // 346.6 us), four in a batch (C4: 50.4 vs 55.0 ms)
     // a batch (HBM-latency bound, work for many waves): UB point pairs per thread
     constexpr int UB = INIM_BATCH_MOVE_U;
     auto kern = bt.B > 1 ? (pairs ? sample_f32_kernel<true, UB, true> : sample_f32_kernel<false, UB, true>)
-                         : (pairs ? sample_f32_kernel<true, 2, false> : sample_f32_kernel<false, 2, false>);
+                         : (pairs ? sample_f32_kernel<true, 2, false> : sample_f32_kernel<false, 1, false>);
     const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair,
-                                 256 * (bt.B > 1 ? UB : 2), bt);
+                                 256 * (bt.B > 1 ? UB : (pairs ? 2 : 1)), bt);
     INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, reinterpret_cast<const float4*>(in), in,
                              reinterpret_cast<float4*>(out), out, n, clip, max_disp, state, splat_next, zn0, zn1,
                              sorted ? 1 : 0, zin, zout, bt.slab));
