@@ -46,13 +46,13 @@ int launch_order_pairs(const double* orig, const double* moved, int64_t n, unsig
 // layout (half the bytes written and gathered, four 8-byte gathers) above 2048^2
 // (measured: 1024^2 paired -5% per iteration; 4096^2 plain -11%), and for plot batches,
 // whose fields stream through HBM.  INIM_PAIRS=0/1 forces either.
-static bool use_pairs(const Geo& g, int B) {
+static bool use_pairs(const Geo& g, bool batched) {
     static int env = -1;
     if (env < 0) {
         const char* e = getenv("INIM_PAIRS");
         env = e ? (e[0] == '0' ? 0 : 1) : 2;
     }
-    return env == 2 ? g.s <= 2048 && B == 1 : env == 1;
+    return env == 2 ? g.s <= 2048 && !batched : env == 1;
 }
 
 // Pixel-order sort of the points inside inim_run (INIM_SORT=0 disables).
@@ -299,7 +299,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         // the move reads the paired field layout (two 16-byte gathers per point) while the
         // field stays L2-resident: one plot up to 2048^2 (INIM_PAIRS overrides); a batch's
         // fields stream through HBM, where the plain (s, s, 2) layout's half bytes win
-        const bool pairs = use_pairs(g, batched ? 2 : 1);
+        const bool pairs = use_pairs(g, batched);
         float* plain = tg ? tg : (pairs ? nullptr : tg_scratch);
         int rc = enqueue_iteration(src, dst, key.n, g, key.ks, key.bg, defect, cur, next, d, plain, exc_at(t),
                                    disp_at(t), key.eps, state, w, mp, st, pairs ? tg_scratch : nullptr, chain, bt,
