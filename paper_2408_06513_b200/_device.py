@@ -79,7 +79,7 @@ def to_device(a, dtype=torch.float32, out: torch.Tensor = None) -> torch.Tensor:
     arr = np.ascontiguousarray(a)
     if dtype == torch.float32:
         # ship float64 as-is and narrow on the device (one cast kernel)
-        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device(), non_blocking=False)
+        src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64)).to(device(), non_blocking=True)
         if out is None:
             out = torch.empty(src.shape, dtype=torch.float32, device=device())
         elif not (out.dtype == torch.float32 and out.is_contiguous() and out.numel() == src.numel()):
