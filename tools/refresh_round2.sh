@@ -19,6 +19,14 @@ ncu --metrics $M --clock-control none --csv --log-file $O/launches_integral.csv 
     python tools/prof_driver.py integral --big > $O/ncu_int.log 2>&1
 PROF_PLOTS=32 PROF_ITERS=10 ncu --metrics $M --clock-control none --csv --log-file $O/launches_splom.csv \
     python tools/prof_driver.py splom > $O/ncu_splom.log 2>&1
-compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_driver.py > $O/sanitize_memcheck.txt 2>&1; echo "exit $?" >> $O/sanitize_memcheck.txt
-compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_driver.py > $O/sanitize_racecheck.txt 2>&1; echo "exit $?" >> $O/sanitize_racecheck.txt
+ATOM=lts__t_requests_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex_op_red.sum,l1tex__t_requests_pipe_lsu_mem_global_op_red.sum,smsp__inst_executed_op_global_red.sum,lts__t_sectors_srcunit_tex_op_red_lookup_hit.sum,lts__t_sectors_srcunit_tex_op_red_lookup_miss.sum,lts__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors_op_red.sum
+PROF_ITERS=2 ncu --set full --import-source on --clock-control none --metrics $ATOM \
+    -k regex:"splat|smooth|lines|chains|write_kernel|sample_f32" --launch-skip 0 -c 9 \
+    -o $O/full_iter_c2 python tools/prof_driver.py iter > $O/ncu_full_c2.log 2>&1
+PROF_ITERS=3 ncu --set full --import-source on --clock-control none --metrics $ATOM \
+    -k regex:"splat_f32|sample_f32|smooth|write_kernel|chains" --launch-skip 0 -c 8 \
+    -o $O/full_iter_c3 python tools/prof_driver.py iter3 > $O/ncu_full_c3.log 2>&1
+PROF_PLOTS=32 PROF_ITERS=3 ncu --set full --import-source on --clock-control none \
+    -k regex:"sample_f32|write_kernel|smooth_v|smooth_h|chains" --launch-skip 10 -c 5 \
+    -o $O/full_splom python tools/prof_driver.py splom > $O/ncu_full_splom.log 2>&1
 ls -la $O
