@@ -688,6 +688,31 @@ def splom_e2e(args, job, world, dist):
                    "pinned float32 host buffers, each rank its own block"}
 
 
+def bench_sweep(args):
+    """BASELINE configs[4]: integral-image-only sweep 512^2 .. 16384^2, fp32, L2 flushed."""
+    import torch
+
+    from paper_2408_06513_b200 import _device as D
+    from paper_2408_06513_b200 import _lib
+
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sampler = ClockSampler(0)
+    sampler.start()
+    rows = bench_integral(lib, D, dev, flush, sizes=tuple(range(9, 15)), reps=max(5, args.steps))
+    clocks = sampler.summary()
+    best = max(rows, key=lambda r: r["frac"])
+    line = {"metric": "integral-image GB/s vs HBM peak (36 B/px: read d, write 8 fp32 tables)",
+            "value": best["GB_s"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": 3,
+            "ms_per_step": best["ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic uniform random textures",
+            "config": {"workload": "integral-image-only sweep 512^2..16384^2 (BASELINE configs[4])",
+                       "best_size": best["size"]},
+            "sweep": rows, "clocks": clocks}
+    print(json.dumps(line), flush=True)
+
+
 def _free_port() -> int:
     import socket
 
