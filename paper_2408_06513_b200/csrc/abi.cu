@@ -17,11 +17,11 @@ int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cuda
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
                       const int* state, cudaStream_t st, bool pairs = false, uint32_t* splat_next = nullptr,
                       float* zn0 = nullptr, float* zn1 = nullptr, bool sorted = false, const Bat& bt = Bat{},
-                      int64_t zin = 0, int64_t zout = 0);
+                      int64_t zin = 0, int64_t zout = 0, bool f32_counts = false);
 int launch_sample_f64(const float* tg, int k, const double* in, double* out, int64_t n, int clip, cudaStream_t st);
 int launch_cast_f64_f32(const double* in, float* out, int64_t count, cudaStream_t st);
 int launch_cast_f32_f64(const float* in, double* out, int64_t count, cudaStream_t st);
-int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
+int launch_smooth_state(const void* in, int in_kind, const Geo& g, const Ws& ws, int kernel_size,
                         float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
                         uint32_t* zero_next = nullptr, const Bat& bt = Bat{});
 int launch_field_from_tables(const float* t8, int k, const double* total, const float* defect, float* targets,
@@ -34,7 +34,7 @@ int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* count
 int launch_unpermute(const float* sorted, const uint32_t* rank, int64_t n, float* out, cudaStream_t st,
                      const Bat& bt = Bat{});
 int launch_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t st,
-                       const Bat& bt = Bat{}, int64_t zout = 0);
+                       const Bat& bt = Bat{}, int64_t zout = 0, bool f32_counts = false);
 int launch_gather_points(const void* pts, int is_f64, const int64_t* rows, const uint32_t* perm, int64_t m,
                          double* out, cudaStream_t st);
 int launch_trust(const double* orig, const double* moved, int64_t n, int nn, unsigned long long* out,
@@ -53,6 +53,17 @@ static bool use_pairs(const Geo& g, bool batched) {
         env = e ? (e[0] == '0' ? 0 : 1) : 2;
     }
     return env == 2 ? g.s <= 2048 && !batched : env == 1;
+}
+
+// Float32 counts with 16-byte reductions in the sorted moves (INIM_F32_COUNTS=0: uint32
+// counts and one reduction per distinct pixel; A/B and the bit-identity test).
+static bool f32_counts_enabled() {
+    static int env = -1;
+    if (env < 0) {
+        const char* e = getenv("INIM_F32_COUNTS");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    return env == 1;
 }
 
 // Pixel-order sort of the points inside inim_run (INIM_SORT=0 disables).
@@ -130,6 +141,8 @@ struct Chain {
     bool splat_next;     // fuse the next iteration's splat into this move
     float *next_exc, *next_disp;
     bool sorted;         // the points are in pixel order (aggregated splat atomics)
+    bool f32_in = false;   // this iteration's counts are float32 (the previous move's 16-byte reductions)
+    bool f32_next = false; // the move splats float32 counts
 };
 
 // One iteration.  `counts` must be zero on entry (or already filled, chain.splatted);
@@ -149,7 +162,8 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
         rc = launch_splat_f32(pts_in, n, g.k, counts, flag, st, max_exc, disp, Bat{bt.B, bt.slab, zin});
         if (rc) return rc;
     }
-    rc = launch_smooth_state(counts, true, g, ws, kernel_size, background, d, true, flag, st, counts_next, bt);
+    rc = launch_smooth_state(counts, chain.f32_in ? 2 : 1, g, ws, kernel_size, background, d, true, flag, st,
+                             counts_next, bt);
     if (rc) return rc;
     rc = launch_carry_scan_state(g, ws, flag, st, bt);
     if (rc) return rc;
@@ -157,9 +171,9 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
     if (rc) return rc;
     uint32_t* sn = chain.splat_next ? counts_next : nullptr;
     rc = pairs ? launch_sample_f32(pairs, g.k, pts_in, pts_out, n, 1, disp, flag, st, true, sn, chain.next_exc,
-                                   chain.next_disp, chain.sorted, bt, zin, zout)
+                                   chain.next_disp, chain.sorted, bt, zin, zout, chain.f32_next)
                : launch_sample_f32(targets, g.k, pts_in, pts_out, n, 1, disp, flag, st, false, sn, chain.next_exc,
-                                   chain.next_disp, chain.sorted, bt, zin, zout);
+                                   chain.next_disp, chain.sorted, bt, zin, zout, chain.f32_next);
     if (rc) return rc;
     if (flag) {
         INIM_CUDA_TRY(launch_pdl(iter_end_kernel, dim3(1), dim3(1), 0, st, (const float*)disp, stop_eps, state));
@@ -259,6 +273,9 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     // moves then gather coalesced field rows and merge their splat atomics, and the
     // final positions (and recorded frames) are scattered back through perm.
     const bool sorted = sort_points_enabled() && key.n >= kSortMinPoints && key.iters >= kSortMinIters;
+    // sorted runs splat the moves' points with 16-byte float reductions (a request per
+    // group of four pixels): float32 counts stay exact integers below 2^24 points
+    const bool f32 = sorted && key.n < ((int64_t)1 << 24) && f32_counts_enabled();
     auto disp_at = [&](int t) { return disp ? disp + t : scratch + 2 * (t & 1); };
     auto exc_at = [&](int t) { return excursions ? excursions + t : scratch + 2 * (t & 1) + 1; };
     if (sorted) {
@@ -295,7 +312,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
         const bool more = t + 1 < key.iters && key.n > 0;
         const bool splat_next = more || (fstats && key.n > 0);
         const Chain chain{t > 0 || sorted, splat_next, more ? exc_at(t + 1) : nullptr,
-                          more ? disp_at(t + 1) : nullptr, sorted};
+                          more ? disp_at(t + 1) : nullptr, sorted, f32 && t > 0, f32};
         // the move reads the paired field layout (two 16-byte gathers per point) while the
         // field stays L2-resident: one plot up to 2048^2 (INIM_PAIRS overrides); a batch's
         // fields stream through HBM, where the plain (s, s, 2) layout's half bytes win
@@ -312,7 +329,7 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
             if (rc) return rc;
         }
         if (fstats && key.n > 0) {
-            rc = launch_frame_stats(next, g.k, fstats + 3 * t, st, bt, 3 * (int64_t)key.iters);
+            rc = launch_frame_stats(next, g.k, fstats + 3 * t, st, bt, 3 * (int64_t)key.iters, f32);
             if (rc) return rc;
         }
         if (nb && key.n > 0) {

@@ -114,8 +114,10 @@ __host__ __device__ inline size_t h_smem_bytes(const HGeo& h, int R) {
 }
 
 // Horizontal pass of tile (bx, by).  zero_next (optional): the other count buffer of
-// the iteration's ping-pong pair; the tile clears its own RH x TWH block of it.
-template <int R, typename T>
+// the iteration's ping-pong pair; the tile clears its own RH x TWH block of it.  CNT:
+// the input is the iteration's counts (uint32, or float32 integers when the move
+// splats with 16-byte float reductions); otherwise a float grid (gaussian_smooth).
+template <int R, typename T, bool CNT = !std::is_same<T, float>::value>
 __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* __restrict__ out, int s, const HGeo& h,
                                               const Taps& taps, uint32_t* __restrict__ zero_next, int bx, int by,
                                               float* hsm) {
@@ -129,7 +131,7 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
     // warps over rows, lanes over columns (coalesced, no index division); every load of
     // a pass is issued before any of its shared-memory stores (up to RPW x NPR loads in
     // flight per thread)
-    constexpr int RPW = std::is_same<T, float>::value ? 4 : 2;  // rows per warp per pass
+    constexpr int RPW = CNT ? 2 : 4;  // rows per warp per pass
     constexpr int NPR = (128 + 2 * R + 31) / 32;  // columns per lane per row (TWH <= 128)
     constexpr int NP4 = (128 + 2 * R + 127) / 128;  // 16-byte groups per lane per row (interior tiles)
     const bool vec = interior && (TWH & 3) == 0 && ((i0 - R) & 3) == 0 && (s & 3) == 0;

@@ -10,8 +10,8 @@
 
 namespace inim {
 
-template <int R, typename T>
-__global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
+template <int R, typename T, bool CNT>
+__global__ void __launch_bounds__(256, CNT ? 4 : 1) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
                                                        uint32_t* __restrict__ zero_next, int64_t zslab) {
     pdl_enter();
@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256, std::is_same<T, float>::value ? 1 : 4) sm
         zero_next = zoff_opt(zero_next, zo);
     }
     extern __shared__ __align__(16) float hsm[];
-    smooth_h_tile<R, T>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
+    smooth_h_tile<R, T, CNT>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
 }
 
 template <int R>
@@ -38,14 +38,14 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
                      blockIdx.y, vsm);
 }
 
-template <int R, typename T>
+template <int R, typename T, bool CNT>
 inline int launch_h(const T* in, float* out, int s, const Taps& taps, const int* state, uint32_t* zero_next,
                     cudaStream_t st, const Bat& bt) {
     const HGeo h = make_hgeo(s);
     const size_t smem = h_smem_bytes(h, R);
-    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_h_kernel<R, T>, 200 * 1024));
+    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_h_kernel<R, T, CNT>, 200 * 1024));
     dim3 grid(s / h.TWH, s / h.RH, bt.B);
-    INIM_CUDA_TRY(launch_pdl(smooth_h_kernel<R, T>, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state,
+    INIM_CUDA_TRY(launch_pdl(smooth_h_kernel<R, T, CNT>, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state,
                              zero_next, bt.slab));
     prof_mark(st, "smooth_h");
     return (int)cudaGetLastError();
@@ -65,13 +65,17 @@ inline int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, cons
     return (int)cudaGetLastError();
 }
 
+// kind: kSmoothGrid (a float grid), kSmoothCountsU32, kSmoothCountsF32 (smooth.cu)
 template <int KS>
-int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg,
+int launch_pair(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt) {
     constexpr int R = 3 * KS;
-    int rc = counts ? launch_h<R, uint32_t>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state, zero_next, st,
-                                            bt)
-                    : launch_h<R, float>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zero_next, st, bt);
+    int rc = kind == 1   ? launch_h<R, uint32_t, true>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state,
+                                                      zero_next, st, bt)
+             : kind == 2 ? launch_h<R, float, true>(static_cast<const float*>(in), ws.tmp, g.s, taps, state,
+                                                   zero_next, st, bt)
+                         : launch_h<R, float, false>(static_cast<const float*>(in), ws.tmp, g.s, taps, state,
+                                                    zero_next, st, bt);
     if (rc) return rc;
     return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st, bt);
 }

@@ -6,6 +6,8 @@
 // atomics, so the results are order-independent and, for identical coordinates,
 // identical to the reference's own integer intermediates.  The host turns them into
 // the reference's floats with the reference's formulas (metrics.py:59,71,112-113,144).
+#include <type_traits>
+
 #include "inim_internal.cuh"
 
 namespace inim {
@@ -32,7 +34,9 @@ INIM_DEV T block_sum(T v, T* red) {
 // nonzero counts.  out[0] += occupied pixels, out[1] += sum over bins of count^2,
 // out[2] += sum of counts (= n).  One thread per bin; each of its four rows is one
 // 16-byte load, consecutive threads read consecutive bins of a row (coalesced).
-__global__ void __launch_bounds__(256) frame_stats_kernel(const uint32_t* __restrict__ counts, int k, u64* out,
+// T: uint32 counts, or float32 counts (exact integers) from the moves' 16-byte reductions
+template <typename T>
+__global__ void __launch_bounds__(256) frame_stats_kernel(const T* __restrict__ counts, int k, u64* out,
                                                           int64_t zslab, int64_t zout) {
     pdl_enter();
     counts = zoff(counts, zslab_off(zslab));  // plot blockIdx.z of a batch
@@ -50,7 +54,10 @@ __global__ void __launch_bounds__(256) frame_stats_kernel(const uint32_t* __rest
             int nz = 0;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const uint4 v = __ldg(row + (size_t)r * (s >> 2));
+                uint4 v = __ldg(row + (size_t)r * (s >> 2));
+                if (std::is_same<T, float>::value)
+                    v = make_uint4((uint32_t)__uint_as_float(v.x), (uint32_t)__uint_as_float(v.y),
+                                   (uint32_t)__uint_as_float(v.z), (uint32_t)__uint_as_float(v.w));
                 bin += v.x + v.y + v.z + v.w;
                 nz += (v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0);
             }
@@ -59,7 +66,7 @@ __global__ void __launch_bounds__(256) frame_stats_kernel(const uint32_t* __rest
             sq += (u64)bin * bin;
         }
     } else if (blockIdx.x == 0 && threadIdx.x < s * s) {  // 1x1 and 2x2 grids: no bins
-        const uint32_t c = counts[threadIdx.x];
+        const uint32_t c = (uint32_t)counts[threadIdx.x];
         occ = c != 0;
         tot = c;
     }
@@ -228,10 +235,15 @@ static unsigned blocks_for(int64_t work, int per_block, int per_sm) {
 }
 
 // zout: u64 between consecutive plots' outputs of a batch
-int launch_frame_stats(const uint32_t* counts, int k, u64* out3, cudaStream_t st, const Bat& bt, int64_t zout) {
+int launch_frame_stats(const uint32_t* counts, int k, u64* out3, cudaStream_t st, const Bat& bt, int64_t zout,
+                       bool f32_counts) {
     const int64_t bins = k >= 2 ? ((int64_t)1 << (2 * k - 4)) : 1;
-    INIM_CUDA_TRY(launch_pdl(frame_stats_kernel, dim3(blocks_for(bins, 256, bt.B > 1 ? 1 : 8), 1, bt.B), dim3(256), 0,
-                             st, counts, k, out3, bt.slab, zout));
+    const dim3 grid(blocks_for(bins, 256, bt.B > 1 ? 1 : 8), 1, bt.B);
+    if (f32_counts)
+        INIM_CUDA_TRY(launch_pdl(frame_stats_kernel<float>, grid, dim3(256), 0, st,
+                                 reinterpret_cast<const float*>(counts), k, out3, bt.slab, zout));
+    else
+        INIM_CUDA_TRY(launch_pdl(frame_stats_kernel<uint32_t>, grid, dim3(256), 0, st, counts, k, out3, bt.slab, zout));
     prof_mark(st, "frame_stats");
     return (int)cudaGetLastError();
 }

@@ -14,6 +14,11 @@
 
 namespace inim {
 
+// 16-byte float reduction (REDG.E.ADD.F32x4): four adjacent counts in one L2 request.
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 // Warp-aggregated integer atomics: lanes hitting the same pixel in one step are
 // merged (__match_any_sync) and the leader issues one red.add for the group.
 __device__ __forceinline__ void splat_one(uint32_t* counts, int pix) {
@@ -149,7 +154,35 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
         for (int u = 0; u < U; ++u)
             if (p0 + u * stride < npair) __stcs(out2 + p0 + u * stride, o[u]);
         if (splat_next && !stopped) {
-            if (agg) {  // points in pixel order: lanes sharing a pixel merge into one red.add
+            if (agg == 2) {
+                // float counts (exact integers below 2^24): lanes whose points fall in the
+                // same aligned group of four pixels merge into ONE 16-byte reduction
+                // (red.global.add.v4.f32), so the L2 sees a request per group, not per
+                // point (the splat's bound is the L2 reduction request rate)
+                const unsigned am = __activemask();
+                const int lane = threadIdx.x & 31;
+                float* fc = reinterpret_cast<float*>(splat_next);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool ok = p0 + u * stride < npair;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int pix = ok ? pixel_of(h ? o[u].w : o[u].y, s) * s + pixel_of(h ? o[u].z : o[u].x, s)
+                                           : -1;
+                        const int g4 = pix >> 2;  // -1 for padding lanes
+                        const unsigned grp = __match_any_sync(am, g4);
+                        const int sub = pix & 3;
+                        const unsigned b1 = __ballot_sync(am, ok && sub == 1);
+                        const unsigned b2 = __ballot_sync(am, ok && sub == 2);
+                        const unsigned b3 = __ballot_sync(am, ok && sub == 3);
+                        if (ok && lane == __ffs(grp) - 1) {
+                            const int c1 = __popc(grp & b1), c2 = __popc(grp & b2), c3 = __popc(grp & b3);
+                            red_add_v4(fc + 4 * (int64_t)g4, (float)(__popc(grp) - c1 - c2 - c3), (float)c1,
+                                       (float)c2, (float)c3);
+                        }
+                    }
+                }
+            } else if (agg) {  // points in pixel order: lanes sharing a pixel merge into one red.add
                 const unsigned am = __activemask();
                 const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -184,7 +217,11 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
         }
         out[2 * (n - 1)] = ox;
         out[2 * (n - 1) + 1] = oy;
-        if (splat_next && !stopped) atomicAdd(splat_next + pixel_of(oy, s) * s + pixel_of(ox, s), 1u);
+        if (splat_next && !stopped) {
+            const int pix = pixel_of(oy, s) * s + pixel_of(ox, s);
+            if (agg == 2) atomicAdd(reinterpret_cast<float*>(splat_next) + pix, 1.f);
+            else atomicAdd(splat_next + pix, 1u);
+        }
     }
     if (max_disp && !stopped) {
         md = warp_max(md);
@@ -498,7 +535,7 @@ int launch_splat_f64(const double* pts, int64_t n, int k, uint32_t* counts, cuda
 // the caller's (B, n, 2) array or the workspace ping-pong buffers).
 int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64_t n, int clip, float* max_disp,
                       const int* state, cudaStream_t st, bool pairs, uint32_t* splat_next, float* zn0, float* zn1,
-                      bool sorted, const Bat& bt, int64_t zin, int64_t zout) {
+                      bool sorted, const Bat& bt, int64_t zin, int64_t zout, bool f32_counts) {
     const int64_t npair = n >> 1;
     // point pairs (16-byte loads) per thread per step, measured per regime (DESIGN.md
     // 4.5): two for one plot on the L2-resident paired field (C2: one 50.6, four 49.2
@@ -512,7 +549,7 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
                                  256 * (bt.B > 1 ? UB : (pairs ? 2 : 1)), bt);
     INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(256), 0, st, tg, k, reinterpret_cast<const float4*>(in), in,
                              reinterpret_cast<float4*>(out), out, n, clip, max_disp, state, splat_next, zn0, zn1,
-                             sorted ? 1 : 0, zin, zout, bt.slab));
+                             sorted ? (f32_counts ? 2 : 1) : 0, zin, zout, bt.slab));
     prof_mark(st, "sample");
     return (int)cudaGetLastError();
 }

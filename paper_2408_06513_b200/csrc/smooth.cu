@@ -141,22 +141,25 @@ void make_taps(int kernel_size, Taps* taps) {
 }
 
 template <int KS>
-int launch_pair(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
+int launch_pair(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
                 int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt);
 
-int launch_smooth_state(const void* in, bool in_is_counts, const Geo& g, const Ws& ws, int kernel_size,
+// in_kind: 0 = a float grid (gaussian_smooth), 1 = uint32 counts, 2 = float32 counts
+// (integers; the move's 16-byte float reductions).  Counts smoothing also clears
+// zero_next for the next iteration.
+int launch_smooth_state(const void* in, int in_kind, const Geo& g, const Ws& ws, int kernel_size,
                         float background, float* d, bool emit_aggregates, const int* state, cudaStream_t st,
                         uint32_t* zero_next, const Bat& bt) {
     if (kernel_size < 1) return INIM_EKERNEL;
     if (3 * kernel_size > kMaxR)
-        return launch_generic(in, in_is_counts, g, ws, kernel_size, background, d, emit_aggregates, state, zero_next,
+        return launch_generic(in, in_kind == 1, g, ws, kernel_size, background, d, emit_aggregates, state, zero_next,
                               st, bt);
     Taps taps;
     make_taps(kernel_size, &taps);
     const int emit = emit_aggregates ? 1 : 0;
     switch (kernel_size) {
 #define INIM_KS(K) \
-    case K: return launch_pair<K>(in, in_is_counts, g, ws, taps, background, d, emit, state, zero_next, st, bt);
+    case K: return launch_pair<K>(in, in_kind, g, ws, taps, background, d, emit, state, zero_next, st, bt);
         INIM_KS(1) INIM_KS(2) INIM_KS(3) INIM_KS(4) INIM_KS(5) INIM_KS(6) INIM_KS(7) INIM_KS(8)
         INIM_KS(9) INIM_KS(10) INIM_KS(11) INIM_KS(12) INIM_KS(13) INIM_KS(14) INIM_KS(15) INIM_KS(16)
 #undef INIM_KS

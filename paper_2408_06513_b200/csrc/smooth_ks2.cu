@@ -2,12 +2,12 @@
 #include "inim_smooth_launch.cuh"
 
 namespace inim {
-template int launch_pair<5>(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
+template int launch_pair<5>(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
                      int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt);
-template int launch_pair<6>(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
+template int launch_pair<6>(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
                      int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt);
-template int launch_pair<7>(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
+template int launch_pair<7>(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
                      int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt);
-template int launch_pair<8>(const void* in, bool counts, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
+template int launch_pair<8>(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg, float* d,
                      int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt);
 }  // namespace inim

@@ -472,3 +472,42 @@ def test_field_layouts_bit_identical(tmp_path, k):
         assert out.returncode == 0, out.stderr[-2000:]
         outs.append(np.load(dst))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("k,n,ks,metrics", [(10, 200_000, 8, False), (8, 70_000, 8, True), (12, 300_000, 5, False),
+                                            (9, 100_000, 20, True)])
+def test_float_counts_bit_identical(tmp_path, k, n, ks, metrics):
+    """Sorted runs splat with 16-byte float reductions into float32 counts (the default);
+    INIM_F32_COUNTS=0 keeps uint32 counts with one reduction per pixel.  Counts are exact
+    integers either way, so the runs (and the per-frame statistics) are bit-identical."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+
+    from conftest import ROOT
+
+    host = clusters(n, k).astype(np.float64)
+    np.save(tmp_path / "in.npy", host)
+    outs = []
+    for mode in ("0", "1"):
+        dst = tmp_path / f"out{mode}.npz"
+        script = textwrap.dedent(f"""
+            import sys
+            sys.path.insert(0, {str(ROOT)!r})
+            import numpy as np
+            import paper_2408_06513_b200 as P
+            host = np.load({str(tmp_path / "in.npy")!r})
+            r = P.run(P.ScatterDataset(positions=host), P.RegularizationParams(k={k}, kernel_size={ks}, iterations=4),
+                      collect_metrics={"'basic'" if metrics else "'none'"}, store_fields=False)
+            m = np.array([[x.binned_stddev, x.overplotting] for x in r.metrics]) if r.metrics else np.zeros((0, 2))
+            np.savez({str(dst)!r}, pos=r.frame(4), m=m)
+        """)
+        f = tmp_path / f"fc{mode}.py"
+        f.write_text(script)
+        out = subprocess.run([sys.executable, str(f)], capture_output=True, text=True, timeout=300,
+                             env=dict(os.environ, INIM_F32_COUNTS=mode))
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(np.load(dst))
+    assert np.array_equal(outs[0]["pos"], outs[1]["pos"])
+    assert np.array_equal(outs[0]["m"], outs[1]["m"])
