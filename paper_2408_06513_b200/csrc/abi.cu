@@ -274,8 +274,9 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     // final positions (and recorded frames) are scattered back through perm.
     const bool sorted = sort_points_enabled() && key.n >= kSortMinPoints && key.iters >= kSortMinIters;
     // sorted runs splat the moves' points with 16-byte float reductions (a request per
-    // group of four pixels): float32 counts stay exact integers below 2^24 points
-    const bool f32 = sorted && key.n < ((int64_t)1 << 24) && f32_counts_enabled();
+    // group of four pixels): float32 counts stay exact integers below 2^24 points.
+    // Measured: C4 -2%, C2 -0.4%; one 4096^2 plot +1.4% (kept on uint32)
+    const bool f32 = sorted && key.n < ((int64_t)1 << 24) && (batched || g.s <= 2048) && f32_counts_enabled();
     auto disp_at = [&](int t) { return disp ? disp + t : scratch + 2 * (t & 1); };
     auto exc_at = [&](int t) { return excursions ? excursions + t : scratch + 2 * (t & 1) + 1; };
     if (sorted) {
