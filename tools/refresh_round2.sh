@@ -20,7 +20,7 @@ ncu --metrics $M --clock-control none --csv --log-file $O/launches_integral.csv 
 PROF_PLOTS=32 PROF_ITERS=10 ncu --metrics $M --clock-control none --csv --log-file $O/launches_splom.csv \
     python tools/prof_driver.py splom > $O/ncu_splom.log 2>&1
 ATOM=lts__t_requests_srcunit_tex_op_red.sum,lts__t_sectors_srcunit_tex_op_red.sum,l1tex__t_requests_pipe_lsu_mem_global_op_red.sum,smsp__inst_executed_op_global_red.sum,lts__t_sectors_srcunit_tex_op_red_lookup_hit.sum,lts__t_sectors_srcunit_tex_op_red_lookup_miss.sum,lts__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_sectors_op_red.sum
-PROF_ITERS=2 ncu --set full --import-source on --clock-control none --metrics $ATOM \
+PROF_ITERS=3 ncu --set full --import-source on --clock-control none --metrics $ATOM \
     -k regex:"splat|smooth|lines|chains|write_kernel|sample_f32" --launch-skip 0 -c 9 \
     -o $O/full_iter_c2 python tools/prof_driver.py iter > $O/ncu_full_c2.log 2>&1
 PROF_ITERS=3 ncu --set full --import-source on --clock-control none --metrics $ATOM \
