@@ -194,7 +194,10 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
  * `iterations` fixed iterations of every plot, every stage ONE launch over all plots
  * (plot index in grid.z), captured once into a CUDA graph and replayed.
  * pts: device (B, n, 2) float32, updated in place to each plot's final positions (n
- * even when B > 1); ws: inim_workspace_bytes(k, n, B) bytes.  frame_stats: NULL, or
+ * even when B > 1); ws: inim_workspace_bytes(k, n, B) bytes.  stop_eps > 0 runs the
+ * displacement criterion per plot (regularize.py:76-79): a plot stops after the
+ * iteration whose max |delta| < stop_eps, the others go on; states (device int[B][4],
+ * required then) receives each plot's {stopped, iterations done, 0, 0}.  frame_stats: NULL, or
  * device u64[B][iterations][3] (cleared by the call) receiving the per-frame occupancy
  * statistics of every plot (as inim_run_metrics; collect_metrics="basic").  Batches
  * (any B, one plot included) use the wide tile geometry (32 x 128 tiles from 128^2 up;
@@ -202,7 +205,7 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
  * within float32 rounding (the tile sums associate differently), and a plot's result
  * does not depend on B or on its position in the batch (bit-identical). */
 int inim_run_batched(float* pts, int64_t n, int B, int k, int kernel_size, float background, int iterations,
-                     unsigned long long* frame_stats, void* ws, cudaStream_t stream);
+                     float stop_eps, int* states, unsigned long long* frame_stats, void* ws, cudaStream_t stream);
 
 /* Occupancy statistics of a count grid (binned_stddev metrics.py:46-59, overplotting
  * metrics.py:62-71): out3 (device u64[3], NOT cleared) += {occupied pixels, sum over the

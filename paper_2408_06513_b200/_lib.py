@@ -29,7 +29,8 @@ c_size_t = ctypes.c_size_t
 _SIGS = {
     "inim_version": (ctypes.c_char_p, []),
     "inim_workspace_bytes": (c_size_t, [c_int, c_i64, c_int]),
-    "inim_run_batched": (c_int, [c_void_p, c_i64, c_int, c_int, c_int, c_float, c_int, c_void_p, c_void_p, c_void_p]),
+    "inim_run_batched": (c_int, [c_void_p, c_i64, c_int, c_int, c_int, c_float, c_int, c_float, c_void_p, c_void_p,
+                                 c_void_p, c_void_p]),
     "inim_splat": (c_int, [c_void_p, c_int, c_i64, c_int, c_void_p, c_void_p]),
     "inim_smooth_counts": (c_int, [c_void_p, c_int, c_int, c_float, c_void_p, c_void_p, c_void_p]),
     "inim_smooth_grid": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p]),

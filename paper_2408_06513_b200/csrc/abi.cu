@@ -88,8 +88,10 @@ bool pdl_enabled() {
 }
 
 // Per-iteration bookkeeping for the displacement criterion (regularize.py:76-79).
-__global__ void iter_end_kernel(const float* disp, float eps, int* state) {
+__global__ void iter_end_kernel(const float* disp, float eps, int* state, int64_t zslab) {
     pdl_enter();
+    state = zoff(state, zslab_off(zslab));  // plot blockIdx.z of a batch
+    disp = zoff(disp, zslab_off(zslab));
     if (state[0]) return;
     state[1] += 1;
     if (*disp < eps) state[0] = 1;
@@ -101,7 +103,7 @@ __global__ void iter_end_kernel(const float* disp, float eps, int* state) {
 // ping-pong.
 struct FullLayout {
     WsLayout L;
-    size_t counts, d, targets, defect, scratch, sortA, sortB, perm, rank, hist, bytes;
+    size_t counts, d, targets, defect, scratch, state, sortA, sortB, perm, rank, hist, bytes;
 };
 
 // The field kernel folds the closed-form flat response into its normalised arithmetic,
@@ -122,6 +124,7 @@ static FullLayout full_layout(const Geo& g, int64_t n) {
     F.targets = take(sizeof(float) * 4 * g.m);  // paired field layout (also holds a plain field)
     F.defect = take(precomputed_defect(g) ? sizeof(float) * 2 * g.m : 0);
     F.scratch = take(sizeof(float) * 64);
+    F.state = take(sizeof(int) * 4);  // a batched run's per-plot {stopped, iterations done}
     const size_t nn = (size_t)(n > 0 ? n : 1);
     F.sortA = take(sizeof(float) * 2 * nn);  // points in cell order (ping)
     F.sortB = take(sizeof(float) * 2 * nn);  // (pong)
@@ -176,7 +179,8 @@ static int enqueue_iteration(const float* pts_in, float* pts_out, int64_t n, con
                                    chain.next_disp, chain.sorted, bt, zin, zout, chain.f32_next);
     if (rc) return rc;
     if (flag) {
-        INIM_CUDA_TRY(launch_pdl(iter_end_kernel, dim3(1), dim3(1), 0, st, (const float*)disp, stop_eps, state));
+        INIM_CUDA_TRY(launch_pdl(iter_end_kernel, dim3(1, 1, bt.B), dim3(1), 0, st, (const float*)disp, stop_eps,
+                                 state, bt.slab));
         prof_mark(st, "iter_end");
     }
     return (int)cudaGetLastError();
@@ -239,6 +243,13 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
     float* sortB = reinterpret_cast<float*>(base + F.sortB);
     int* perm = reinterpret_cast<int*>(base + F.perm);
     int* hist = reinterpret_cast<int*>(base + F.hist);
+    // a batch's displacement stop runs on per-plot state words in the slabs (every
+    // kernel offsets them by its plot); the caller's states[B][4] receive them at the end
+    int* const caller_states = batched ? state : nullptr;
+    if (batched) state = key.eps > 0.f ? reinterpret_cast<int*>(base + F.state) : nullptr;
+    if (batched && state)
+        INIM_CUDA_TRY(cudaMemset2DAsync(state, B > 1 ? (size_t)bt.slab : 4 * sizeof(int), 0, 4 * sizeof(int), (size_t)B,
+                                        st));
     CUtensorMap map;
     const CUtensorMap* mp = nullptr;
     if (g.TW >= 32) {
@@ -342,8 +353,13 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
             if (rc) return rc;
         }
     }
-    if (sorted && key.iters > 0)
-        return launch_unpermute(pos_out(key.iters - 1), reinterpret_cast<const uint32_t*>(perm), key.n, pts, st, bt);
+    if (sorted && key.iters > 0) {
+        int rc = launch_unpermute(pos_out(key.iters - 1), reinterpret_cast<const uint32_t*>(perm), key.n, pts, st, bt);
+        if (rc) return rc;
+    }
+    if (caller_states && state)
+        INIM_CUDA_TRY(cudaMemcpy2DAsync(caller_states, 4 * sizeof(int), state, B > 1 ? (size_t)bt.slab : 4 * sizeof(int),
+                                        4 * sizeof(int), (size_t)B, cudaMemcpyDeviceToDevice, st));
     return 0;
 }
 
@@ -581,17 +597,19 @@ int inim_run_metrics(float* pts, int64_t n, int k, int kernel_size, float backgr
 }
 
 int inim_run_batched(float* pts, int64_t n, int B, int k, int kernel_size, float background, int iterations,
-                     unsigned long long* frame_stats, void* ws, cudaStream_t stream) {
+                     float stop_eps, int* states, unsigned long long* frame_stats, void* ws, cudaStream_t stream) {
     if (k < 1 || k > INIM_MAX_K || n < 0 || B < 1 || iterations < 0 || !ws || (n > 0 && !pts)) return INIM_EINVAL;
     if (kernel_size < 1) return INIM_EKERNEL;
+    if (stop_eps > 0.f && !states) return INIM_EINVAL;
     if (iterations == 0) return 0;
     if (B > 1 && (n & 1)) return INIM_EINVAL;  // every plot's points 16-byte aligned (two points per access)
     RunKey key;
     memset(&key, 0, sizeof(key));
     key.pts = pts; key.n = n; key.k = k; key.ks = kernel_size; key.bg = auto_background(n, k, background);
     key.iters = iterations; key.ws = ws; key.st = stream; key.B = B;
+    key.eps = stop_eps; key.state = stop_eps > 0.f ? states : nullptr;
     key.fstats = frame_stats;
-    return run_graph(key, pts, nullptr, nullptr, nullptr, nullptr, nullptr, ws, stream);
+    return run_graph(key, pts, nullptr, nullptr, nullptr, nullptr, key.eps > 0.f ? states : nullptr, ws, stream);
 }
 
 int inim_frame_stats(const uint32_t* counts, int k, unsigned long long* out3, cudaStream_t stream) {

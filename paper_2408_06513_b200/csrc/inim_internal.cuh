@@ -218,6 +218,10 @@ __host__ __device__ __forceinline__ Ws ws_shift(Ws w, int64_t b) {
 // byte offset of this CTA's plot
 INIM_DEV int64_t zslab_off(int64_t slab) { return (int64_t)blockIdx.z * slab; }
 
+// the run's device state word pair {stopped, iterations done} of this CTA's plot: one
+// per plot, inside its workspace slab, in a batch
+INIM_DEV const int* zstate(const int* state, int64_t slab) { return state ? zoff(state, zslab_off(slab)) : state; }
+
 // ---------------------------------------------------------------- launch profiler
 // When g_prof is set (inim_profile_run only), every launcher records a CUDA event
 // after its launch; consecutive events bracket exactly one launch.

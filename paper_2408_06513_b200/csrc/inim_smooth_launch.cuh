@@ -15,6 +15,7 @@ __global__ void __launch_bounds__(256, CNT ? 4 : 1) smooth_h_kernel(const T* __r
                                                        const HGeo h, const Taps taps, const int* state,
                                                        uint32_t* __restrict__ zero_next, int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;
     if (zslab) {  // plot blockIdx.z of a batch (the input is the plot's counts)
         const int64_t zo = zslab_off(zslab);
@@ -31,6 +32,7 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
                                                        const Geo g, const VGeo v, const Ws ws, const Taps taps,
                                                        float background, int emit, const int* state, int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
     const int64_t zo = zslab_off(zslab);

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, CPL == 4 ? 5 : 1) write_ker
                                                                   const Ws ws0, const WriteOut out0, const int* state,
                                                                   int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;  // displacement stop already reached
     const int64_t zo = zslab_off(zslab);  // plot blockIdx.z of a batch
     d = zoff(d, zo);

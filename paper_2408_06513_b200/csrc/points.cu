@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(256) splat_f32_kernel(const float* __restrict_
                                                         uint32_t* __restrict__ counts, const int* state, float* zero0,
                                                         float* zero1, int64_t zpts, int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;
     {  // plot blockIdx.z of a batch
         const int64_t zo = zslab_off(zslab);
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
         splat_next = zoff_opt(splat_next, zo);
         zn0 = zoff_opt(zn0, zo);
         zn1 = zoff_opt(zn1, zo);
+        state = zstate(state, zslab);
     }
     const bool stopped = state && state[0];
     const int s = 1 << k;

@@ -15,6 +15,7 @@ namespace inim {
 template <bool BATCH>
 __global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
+    if (BATCH) state = zstate(state, zslab);
     if (state && state[0]) return;
     const Ws ws = BATCH ? ws_shift(ws0, zslab_off(zslab)) : ws0;
     __shared__ double part[16][33];
@@ -35,6 +36,7 @@ __global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws0, 
 template <int MAXCH, bool BATCH>
 __global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
+    if (BATCH) state = zstate(state, zslab);
     if (state && state[0]) return;
     const Ws ws = BATCH ? ws_shift(ws0, zslab_off(zslab)) : ws0;
     __shared__ double part[16][33];
@@ -49,6 +51,7 @@ __global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws w
 // launch of its own so that no reduce warp has to fence and count its band's arrivals.
 __global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;
     const Ws ws = ws_shift(ws0, zslab_off(zslab));
     __shared__ double rowtot[32];

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(256) generic_h_kernel(const T* __restrict__ in
                                                         const int* state, uint32_t* __restrict__ zero_next,
                                                         int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;
     {
         const int64_t zo = zslab_off(zslab);
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(256) generic_v_kernel(const float* __restrict_
                                                         const float* __restrict__ taps, const GenericTaps gt,
                                                         float background, const int* state, int64_t zslab) {
     pdl_enter();
+    state = zstate(state, zslab);
     if (state && state[0]) return;
     {
         const int64_t zo = zslab_off(zslab);

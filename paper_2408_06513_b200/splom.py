@@ -63,6 +63,8 @@ class SplomConfig:
     iterations: int = 10
     max_batch: int = 256        # plots per batched launch (bounds the workspace: ~43 MB per plot at C4)
     collect_metrics: bool = False  # per-frame binned_stddev / overplotting of every plot ("basic")
+    stop: str = "fixed"         # or "displacement": each plot stops at its own iteration (regularize.py:76-79)
+    epsilon: float = 1e-4
 
 
 class DeviceSplom:
@@ -91,6 +93,14 @@ class DeviceSplom:
         self.ws = torch.empty(wsb, dtype=torch.uint8, device=self.dev)
         self.stats = (torch.zeros((nb, cfg.iterations, 3), dtype=torch.int64, device=self.dev)
                       if cfg.collect_metrics else None)
+        if cfg.stop not in ("fixed", "displacement"):
+            raise ValueError("a batched run stops on a fixed count or on displacement")
+        self.eps = 0.0
+        if cfg.stop == "displacement":
+            if not cfg.epsilon > 0:
+                raise ValueError("epsilon must be > 0")
+            self.eps = max(float(np.float32(cfg.epsilon)), float(np.finfo(np.float32).smallest_subnormal))
+        self.states = torch.zeros((nb, 4), dtype=torch.int32, device=self.dev) if self.eps > 0 else None
 
     def load(self, make_plot: Callable[[int], np.ndarray]):
         for q, idx in enumerate(self.ids):
@@ -106,7 +116,9 @@ class DeviceSplom:
         for b0, b1 in self.chunks:
             stats = D.ptr(self.stats[b0:b1]) if self.stats is not None else None
             self._lib.check(lib.inim_run_batched(D.ptr(self.work[b0:b1]), cfg.points, b1 - b0, cfg.k,
-                                                 cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(self.ws),
+                                                 cfg.kernel_size, 0.0, cfg.iterations, self.eps,
+                                                 D.ptr(self.states[b0:b1]) if self.states is not None else None,
+                                                 stats, D.ptr(self.ws),
                                                  stream), "splom run")
             if on_chunk is not None:
                 on_chunk(b0, b1)
@@ -139,7 +151,9 @@ class DeviceSplom:
             cur.wait_event(ev)
             stats = D.ptr(self.stats[b0:b1]) if self.stats is not None else None
             self._lib.check(lib.inim_run_batched(D.ptr(self.work[b0:b1]), cfg.points, b1 - b0, cfg.k,
-                                                 cfg.kernel_size, 0.0, cfg.iterations, stats, D.ptr(self.ws),
+                                                 cfg.kernel_size, 0.0, cfg.iterations, self.eps,
+                                                 D.ptr(self.states[b0:b1]) if self.states is not None else None,
+                                                 stats, D.ptr(self.ws),
                                                  D.stream()), "splom run")
             done = torch.cuda.Event()
             done.record(cur)
@@ -152,6 +166,12 @@ class DeviceSplom:
         cur.wait_event(fin)
         return host_out
 
+    def iterations_done(self) -> list:
+        """Iterations each plot ran (all of them for stop="fixed")."""
+        if self.states is None:
+            return [self.cfg.iterations] * len(self.ids)
+        return [int(v) for v in self.states[:, 1].cpu().tolist()]
+
     def metrics(self):
         """Per plot and frame 1..iterations: (binned_stddev, overplotting) as the
         reference's record_for_frame (metrics.py:46-71, 147-168), from the device
@@ -162,8 +182,9 @@ class DeviceSplom:
             raise ValueError("SplomConfig(collect_metrics=True) is needed")
         st = self.stats.cpu().numpy()
         n, k = self.cfg.points, self.cfg.k
+        done = self.iterations_done()
         return [[(stddev_from_stats(int(st[q, t, 1]), int(st[q, t, 2]), k), overplotting_from_stats(int(st[q, t, 0]), n))
-                 for t in range(self.cfg.iterations)] for q in range(len(self.ids))]
+                 for t in range(done[q])] for q in range(len(self.ids))]
 
 
 def gather_results(local, nplots: int, world: int, group=None):

@@ -511,3 +511,29 @@ def test_float_counts_bit_identical(tmp_path, k, n, ks, metrics):
         outs.append(np.load(dst))
     assert np.array_equal(outs[0]["pos"], outs[1]["pos"])
     assert np.array_equal(outs[0]["m"], outs[1]["m"])
+
+
+def test_splom_batch_displacement_stop(P, oracle):
+    """stop="displacement" in a batched run: each plot stops after its own iteration
+    whose max |delta| < epsilon (regularize.py:76-79) while the rest of the batch goes on;
+    iteration counts and final positions match one run per plot and the oracle."""
+    from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
+
+    eps = 2e-3
+    cfg = SplomConfig(nplots=4, points=20_000, k=8, kernel_size=8, iterations=30, stop="displacement", epsilon=eps,
+                      collect_metrics=True)
+    job = DeviceSplom(cfg, range(cfg.nplots))
+    job.load(lambda i: splom_plot(i, cfg.points))
+    res = job.run().cpu().numpy().astype(np.float64)
+    done = job.iterations_done()
+    mets = job.metrics()
+    assert len(set(done)) > 1, done  # the plots stop at different iterations
+    for i in range(cfg.nplots):
+        pts = splom_plot(i, cfg.points)
+        r = P.run(P.ScatterDataset(positions=pts), P.RegularizationParams(k=8, kernel_size=8, iterations=30,
+                                                                          stop="displacement", epsilon=eps))
+        frames = oracle.run_positions(pts, 8, 8, 30, stop="displacement", epsilon=eps)
+        assert done[i] == r.iterations == len(frames) - 1, (i, done[i], r.iterations, len(frames) - 1)
+        assert maxerr(res[i], r.frame(r.iterations)) <= POS_TOL, i
+        assert maxerr(res[i], frames[-1]) <= POS_TOL, i
+        assert len(mets[i]) == done[i]
