@@ -519,7 +519,7 @@ def test_splom_batch_displacement_stop(P, oracle):
     iteration counts and final positions match one run per plot and the oracle."""
     from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
 
-    eps = 2e-3
+    eps = 0.019  # the oracle's displacements cross it at iterations 9, 9, 9, 10 (margins >= 6e-4)
     cfg = SplomConfig(nplots=4, points=20_000, k=8, kernel_size=8, iterations=30, stop="displacement", epsilon=eps,
                       collect_metrics=True)
     job = DeviceSplom(cfg, range(cfg.nplots))
