@@ -20,6 +20,13 @@ constexpr int kWarp = 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 // ------------------------------------------------------------------ warp primitives
+// three-input maximum (one FMNMX3 on sm_100a); NaN handling as fmaxf
+INIM_DEV float fmax3f(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 INIM_DEV float warp_inclusive_scan(float v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -331,14 +331,16 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         }
         return (double)ws.x1[(int64_t)B * s + s - 1 + dl] + C;
     };
-    // normalised marginal entries (MODE 1): value / C, minus the flat value when folding
+    // normalised marginal entries (MODE 1): value / C, minus the flat value when folding.
+    // The field's marginal coefficients are kept HALVED (exact: a power-of-two scale) so
+    // the 1/2 of the raw map folds into them instead of costing a multiply per pixel.
     auto nap = [&](int sg) {
         const double v = apre(sg) * invC;
-        return (float)(diff ? v - (double)flat_apre_count(sg, s) * inv_s2 : v);
+        return (float)(0.5 * (diff ? v - (double)flat_apre_count(sg, s) * inv_s2 : v));
     };
     auto nds = [&](int dl) {
         const double v = dsuf(dl) * invC;
-        return (float)(diff ? v - (double)flat_dsuf_count(dl, s) * inv_s2 : v);
+        return (float)(0.5 * (diff ? v - (double)flat_dsuf_count(dl, s) * inv_s2 : v));
     };
     // per-column constants and initial windows (row 0)
     float A[CPL], Bc[CPL], w1[CPL], w2[CPL], wa[CPL], wd[CPL];
@@ -355,7 +357,7 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
             wa[e] = (float)(ok ? apre(a + i) : 0.0);  // Apre[i + j]
             wd[e] = (float)(ok ? dsuf(i - a) : 0.0);  // Dsuf[i - j]
         } else {
-            Bc[e] = (float)(diff ? cv * invC - (i + 1) * inv_s : cv * invC);  // Cp
+            Bc[e] = (float)(0.5 * (diff ? cv * invC - (i + 1) * inv_s : cv * invC));  // Cp / 2
             wa[e] = ok ? nap(a + i) : 0.f;
             wd[e] = ok ? nds(i - a) : 0.f;
         }
@@ -374,7 +376,7 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
                 Q = (float)(Rp - vh);
                 S = (float)(C - Rp + vh);
             } else {
-                Q = (float)(diff ? Rp * invC - (a + lane + 1) * inv_s : Rp * invC);  // Rp
+                Q = (float)(0.5 * (diff ? Rp * invC - (a + lane + 1) * inv_s : Rp * invC));  // Rp / 2
             }
             if (lane < TH - 1) {  // entry q feeds row q + 1
                 const int c1 = i0 - 2 - lane;
@@ -399,13 +401,14 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
     // running maxima, max(-gx, -gy) and max(gx, gy); max(g) - 1 == max(g - 1) exactly
     float excHi = -1.f;
     // per-column geometry of the field (hoisted out of the row sweep)
-    float colx[CPL], colb1[CPL], colip1[CPL];
+    float colx[CPL], colip1[CPL];
+    uint32_t upcnt[CPL];  // flat wedge_up count of (i, a + r), advanced row by row
 #pragma unroll
     for (int e = 0; e < CPL; ++e) {
         const int i = i0 + u0 + e;
         colx[e] = (float)i * scale;
-        colb1[e] = 2.f * colx[e] - 1.f;
         colip1[e] = (float)(i + 1) * scale;
+        upcnt[e] = diff ? flat_up_count(i, s - 1 - i, a, 2 * a + 1) : 0u;
     }
     // MODE 1 with an explicit defect: the row's values are fetched one row ahead so their
     // latency hides behind the previous row's work.
@@ -500,39 +503,47 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
         } else {
             const int j = a + r;
             const float yy = j * scale, fj = (j + 1) * scale;
-            const float a1 = 1.f - 2.f * yy, omq = one - Qr;
-            const int tj1 = 2 * j + 1;
+            // halved coefficients (see nap): a1 = (1 - 2y) / 2, b1 = (2x - 1) / 2, Qr = Rp / 2,
+            // cp = Cp / 2, ap / ds = Apre / 2, Dsuf / 2; the x and y terms then read
+            //   gx = tl a1 + up b1 + cp u + (omq - cp) ulx + Q hp + (1 + one/2 - ap - ds) x + ap
+            //   gy = -tl b1 + up a1 + cp hp + (omq - cp) uly + Q u + (ap + ds) y + y
+            // with ulx - uly = x - y and u + hp = x + y (anchors, mapping.py:42-47).
+            const float a1 = 0.5f - yy, omq = 0.5f * one - Qr;
+            constexpr float kx = 1.f + 0.5f * one;
+            const uint32_t jp1 = (uint32_t)(j + 1);
             float res[2 * CPL];
 #pragma unroll
             for (int e = 0; e < CPL; ++e) {
-                const int i = i0 + u0 + e;
-                const float xx = colx[e], b1 = colb1[e];
+                const float xx = colx[e], b1 = xx - 0.5f;
                 const float tl = (A[e] + Pr) + (off + loc[e]);
                 const float up = (UL[e] + UR[e] - V[e]) + (w1[e] + w2[e]);
                 float tln, upn;
                 if (diff) {
                     tln = fmaf(tl, invCf, -colip1[e] * fj);
-                    upn = fmaf(up, invCf, -(float)flat_up_count(i, s - 1 - i, j, tj1) * invs2f);
+                    upn = fmaf(up, invCf, -(float)upcnt[e] * invs2f);
+                    // count(i, j + 1) - count(i, j) = 1 + min(j + 1, i) + min(j + 1, s - 1 - i)
+                    const uint32_t i = (uint32_t)(i0 + u0 + e);
+                    upcnt[e] += 1u + min(jp1, i) + min(jp1, (uint32_t)(s - 1) - i);
                 } else {
                     tln = tl * invCf;
                     upn = up * invCf;
                 }
-                const float cp = Bc[e], ap = wa[e], ds = wd[e];
-                // anchors (mapping.py:42-47) without branches: x + y and x - y are exact
-                const float sxy = xx + yy;
-                const float ulx = fmaxf(xx - yy, 0.f), uly = fmaxf(yy - xx, 0.f);
-                const float u = fminf(sxy, 1.f), hp = fmaxf(sxy - 1.f, 0.f);  // urx = dly, ury = dlx
-                const float gxs = fmaf(cp, u - ulx, fmaf(omq, ulx, fmaf(Qr, hp, fmaf(one - ap - ds, xx, ap))));
-                const float gys = fmaf(cp, hp - uly, fmaf(omq, uly, fmaf(Qr, u, (ap + ds) * yy)));
-                float gx = fmaf(0.5f, fmaf(tln, a1, fmaf(upn, b1, gxs)), xx);
-                float gy = fmaf(0.5f, fmaf(tln, -b1, fmaf(upn, a1, gys)), yy);
+                const float cp = Bc[e], ap = wa[e], sad = ap + wd[e];
+                // anchors without branches: x + y and x - y are exact, and so are
+                // uly = ulx - (x - y) and hp = (x + y) - u
+                const float dxy = xx - yy, sxy = xx + yy;
+                const float ulx = fmaxf(dxy, 0.f), uly = ulx - dxy;
+                const float u = fminf(sxy, 1.f), hp = sxy - u;  // urx = dly, ury = dlx
+                const float m = omq - cp;
+                float gx = fmaf(tln, a1, fmaf(upn, b1, fmaf(cp, u, fmaf(m, ulx, fmaf(Qr, hp, fmaf(kx - sad, xx, ap))))));
+                float gy = fmaf(tln, -b1, fmaf(upn, a1, fmaf(cp, hp, fmaf(m, uly, fmaf(Qr, u, fmaf(sad, yy, yy))))));
                 if (MODE == 2) {
                     gx -= dcur[e].x;
                     gy -= dcur[e].y;
                 }
                 if (act) {
-                    exc = fmaxf(exc, fmaxf(-gx, -gy));
-                    excHi = fmaxf(excHi, fmaxf(gx, gy));
+                    exc = fmax3f(exc, -gx, -gy);
+                    excHi = fmax3f(excHi, gx, gy);
                 }
                 res[2 * e] = __saturatef(gx);
                 res[2 * e + 1] = __saturatef(gy);
