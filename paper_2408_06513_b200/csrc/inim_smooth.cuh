@@ -52,11 +52,11 @@ __device__ __forceinline__ void fir_line(const Taps& taps, int n, Load line, Sto
     }
 }
 
-// The same FIR with the input line read as float4 (inputs 4*q4 .. 4*q4 + 3): n is a
-// multiple of P, P a multiple of 4, and line4 may read up to 3 floats past the last
-// input (they are never used).
-template <int R, int P, typename Load4, typename Store>
-__device__ __forceinline__ void fir_line4(int n, Load4 line4, Store store) {
+// The same FIR with the input line read as float4 (inputs 4*q4 .. 4*q4 + 3) and the
+// outputs stored four at a time: n is a multiple of P, P a multiple of 4, and line4 may
+// read up to 3 floats past the last input (they are never used).
+template <int R, int P, typename Load4, typename Store4>
+__device__ __forceinline__ void fir_line4(int n, Load4 line4, Store4 store4) {
     constexpr int NT = 2 * R + 1;
     constexpr int NQ = P + NT - 1;
     constexpr int NQ4 = (NQ + 3) / 4;
@@ -79,7 +79,7 @@ __device__ __forceinline__ void fir_line4(int n, Load4 line4, Store store) {
             }
         }
 #pragma unroll
-        for (int pp = 0; pp < P; ++pp) store(p0 + pp, acc[pp]);
+        for (int pp = 0; pp < P; pp += 4) store4(p0 + pp, make_float4(acc[pp], acc[pp + 1], acc[pp + 2], acc[pp + 3]));
     }
 }
 
@@ -103,31 +103,45 @@ inline HGeo make_hgeo(int s) {
 // of fir_line4 run up to 3 past the line), a multiple of 4 with pitch/4 odd, so that
 // the 16-byte row stores and the 16-byte per-row FIR reads (lane = row) are both free
 // of bank conflicts.
-__host__ __device__ inline int h_pitch(const HGeo& h, int R) {
-    int p = (h.TWH + 2 * R + 3 + 3) & ~3;
+__host__ __device__ inline int h_pitch(int TWH, int R) {
+    int p = (TWH + 2 * R + 3 + 3) & ~3;
+    if (((p >> 2) & 1) == 0) p += 4;
+    return p;
+}
+
+// Row pitch of the output staging tile: a multiple of 4 with pitch/4 odd (16-byte FIR
+// stores, lane = row, and 16-byte row reads are conflict-free); TWH + 1 when the tile
+// is narrower than a 16-byte group.
+__host__ __device__ inline int h_opitch(int TWH) {
+    if (TWH & 3) return TWH + 1;
+    int p = TWH + 4;
     if (((p >> 2) & 1) == 0) p += 4;
     return p;
 }
 
 __host__ __device__ inline size_t h_smem_bytes(const HGeo& h, int R) {
-    return ((size_t)h.RH * h_pitch(h, R) + (size_t)h.RH * (h.TWH + 1)) * sizeof(float);
+    return ((size_t)h.RH * h_pitch(h.TWH, R) + (size_t)h.RH * h_opitch(h.TWH)) * sizeof(float);
 }
 
 // Horizontal pass of tile (bx, by).  zero_next (optional): the other count buffer of
 // the iteration's ping-pong pair; the tile clears its own RH x TWH block of it.  CNT:
 // the input is the iteration's counts (uint32, or float32 integers when the move
 // splats with 16-byte float reductions); otherwise a float grid (gaussian_smooth).
-template <int R, typename T, bool CNT = !std::is_same<T, float>::value>
+// FULL: the geometry every grid of side >= 128 gets (32 x 128 tiles, 8 warps) as
+// compile-time constants, so the staging, clearing and store loops fold to straight
+// code (the runtime-geometry form spent ~40% of the kernel's instructions on them).
+template <int R, typename T, bool CNT = !std::is_same<T, float>::value, bool FULL = false>
 __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* __restrict__ out, int s, const HGeo& h,
                                               const Taps& taps, uint32_t* __restrict__ zero_next, int bx, int by,
                                               float* hsm) {
-    const int RH = h.RH, TWH = h.TWH, ld = h_pitch(h, R);
-    float* sh = hsm;                      // [RH][ld]         input rows (row-major)
-    float* so = hsm + (size_t)RH * ld;    // [RH][TWH + 1]    output staging
+    const int RH = FULL ? 32 : h.RH, TWH = FULL ? 128 : h.TWH, NWH = FULL ? 8 : h.NWH, CW = FULL ? 16 : h.CW;
+    const int ld = h_pitch(TWH, R), op = h_opitch(TWH);
+    float* sh = hsm;                      // [RH][ld]  input rows (row-major)
+    float* so = hsm + (size_t)RH * ld;    // [RH][op]  output staging
     const int j0 = by * RH, i0 = bx * TWH;
     const int W = TWH + 2 * R;
     const bool interior = i0 - R >= 0 && i0 + TWH + R <= s;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = FULL ? 8 : (int)(blockDim.x >> 5);
     // warps over rows, lanes over columns (coalesced, no index division); every load of
     // a pass is issued before any of its shared-memory stores (up to RPW x NPR loads in
     // flight per thread)
@@ -195,9 +209,9 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
             for (int q = 0; q < RPW; ++q) {
                 const int r = r0 + q * nw;
                 if (r >= RH) break;
-                if ((TWH & 3) == 0) {
+                if ((TWH & 3) == 0) {  // TWH <= 128: at most one 16-byte group per lane
                     uint4* z4 = reinterpret_cast<uint4*>(zero_next + (int64_t)(j0 + r) * s + i0);
-                    for (int c4 = lane; c4 < (TWH >> 2); c4 += 32) z4[c4] = make_uint4(0u, 0u, 0u, 0u);
+                    if (lane < (TWH >> 2)) z4[lane] = make_uint4(0u, 0u, 0u, 0u);
                 } else {
                     for (int c = lane; c < TWH; c += 32) zero_next[(int64_t)(j0 + r) * s + i0 + c] = 0u;
                 }
@@ -205,27 +219,30 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
         }
     }
     __syncthreads();
-    if (lane < RH && w < h.NWH) {
-        const int c0 = w * h.CW;
+    if (lane < RH && w < NWH) {
+        const int c0 = w * CW;
         const float* row = sh + lane * ld + c0;
-        auto store = [&](int p, float v) { so[lane * (TWH + 1) + c0 + p] = v; };
-        if ((h.CW & 15) == 0) {  // 16-byte reads of the row (c0 and ld are multiples of 4)
-            fir_line4<R, 16>(h.CW, [&](int q4) { return *reinterpret_cast<const float4*>(row + 4 * q4); }, store);
+        float* orow = so + lane * op + c0;
+        if ((CW & 15) == 0) {  // 16-byte reads of the row and 16-byte stores of the outputs
+            fir_line4<R, 16>(CW, [&](int q4) { return *reinterpret_cast<const float4*>(row + 4 * q4); },
+                             [&](int p, float4 v) { *reinterpret_cast<float4*>(orow + p) = v; });
         } else {
-            fir_line<R, 16>(taps, h.CW, [&](int q) { return row[q]; }, store);
+            fir_line<R, 16>(taps, CW, [&](int q) { return row[q]; }, [&](int p, float v) { orow[p] = v; });
         }
     }
     __syncthreads();
-    if ((TWH & 3) == 0) {  // 16-byte stores of the output tile
-        const int TW4 = TWH >> 2, l4 = 31 - __clz(TW4);  // TWH is a power of two
-        for (int q = threadIdx.x; q < RH * TW4; q += blockDim.x) {
+    if ((TWH & 3) == 0) {  // 16-byte row reads of the staging tile, 16-byte stores
+        const int TW4 = TWH >> 2, l4 = FULL ? 5 : 31 - __clz(TW4);  // TWH is a power of two
+        float* obase = out + (int64_t)j0 * s + i0;
+        const int nthr = FULL ? 256 : (int)blockDim.x;
+#pragma unroll 4
+        for (int q = threadIdx.x; q < RH * TW4; q += nthr) {
             const int r = q >> l4, c = 4 * (q & (TW4 - 1));
-            const float* sr = so + r * (TWH + 1) + c;
-            *reinterpret_cast<float4*>(out + (int64_t)(j0 + r) * s + i0 + c) = make_float4(sr[0], sr[1], sr[2], sr[3]);
+            *reinterpret_cast<float4*>(obase + (int64_t)r * s + c) = *reinterpret_cast<const float4*>(so + r * op + c);
         }
     } else {
         for (int r = w; r < RH; r += nw)
-            for (int c = lane; c < TWH; c += 32) out[(int64_t)(j0 + r) * s + i0 + c] = so[r * (TWH + 1) + c];
+            for (int c = lane; c < TWH; c += 32) out[(int64_t)(j0 + r) * s + i0 + c] = so[r * op + c];
     }
     __syncthreads();  // the tile's shared memory may be reused by the caller's next tile
 }

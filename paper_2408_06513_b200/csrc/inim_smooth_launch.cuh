@@ -10,7 +10,7 @@
 
 namespace inim {
 
-template <int R, typename T, bool CNT>
+template <int R, typename T, bool CNT, bool FULL>
 __global__ void __launch_bounds__(256, CNT ? 4 : 1) smooth_h_kernel(const T* __restrict__ in, float* __restrict__ out, int s,
                                                        const HGeo h, const Taps taps, const int* state,
                                                        uint32_t* __restrict__ zero_next, int64_t zslab) {
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(256, CNT ? 4 : 1) smooth_h_kernel(const T* __r
         zero_next = zoff_opt(zero_next, zo);
     }
     extern __shared__ __align__(16) float hsm[];
-    smooth_h_tile<R, T, CNT>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
+    smooth_h_tile<R, T, CNT, FULL>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
 }
 
 template <int R>
@@ -45,10 +45,12 @@ inline int launch_h(const T* in, float* out, int s, const Taps& taps, const int*
                     cudaStream_t st, const Bat& bt) {
     const HGeo h = make_hgeo(s);
     const size_t smem = h_smem_bytes(h, R);
-    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_h_kernel<R, T, CNT>, 200 * 1024));
+    // grids of side >= 128 all get the 32 x 128 x 8-warp geometry: compile it in
+    const bool full = h.RH == 32 && h.TWH == 128 && h.NWH == 8;
+    auto kern = full ? smooth_h_kernel<R, T, CNT, true> : smooth_h_kernel<R, T, CNT, false>;
+    INIM_CUDA_TRY(ensure_smem_limit((const void*)kern, 200 * 1024));
     dim3 grid(s / h.TWH, s / h.RH, bt.B);
-    INIM_CUDA_TRY(launch_pdl(smooth_h_kernel<R, T, CNT>, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state,
-                             zero_next, bt.slab));
+    INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(h.NWH * 32), smem, st, in, out, s, h, taps, state, zero_next, bt.slab));
     prof_mark(st, "smooth_h");
     return (int)cudaGetLastError();
 }
