@@ -10,6 +10,9 @@
 #ifndef INIM_FFMA2_V
 #define INIM_FFMA2_V 1  // vertical pass on packed fma.rn.f32x2 (0: scalar FFMA immediates)
 #endif
+#ifndef INIM_FFMA2_H
+#define INIM_FFMA2_H 1  // horizontal pass on packed fma.rn.f32x2 (0: scalar FFMA immediates)
+#endif
 #include "inim_tiles.cuh"
 
 namespace inim {
@@ -80,6 +83,53 @@ __device__ __forceinline__ void fir_line4(int n, Load4 line4, Store4 store4) {
         }
 #pragma unroll
         for (int pp = 0; pp < P; pp += 4) store4(p0 + pp, make_float4(acc[pp], acc[pp + 1], acc[pp + 2], acc[pp + 3]));
+    }
+}
+
+// fir_line4 on packed fma.rn.f32x2: outputs (2m, 2m + 1) form one accumulator pair, and
+// input x[i] enters it as a broadcast operand (ptxas encodes the {x, x} pair as `R.F32`,
+// no moves) times the shifted tap pair (w[i - 2m], w[i - 2m - 1]) from constant memory
+// (uniform registers; zero outside the kernel).  Each output still accumulates
+// fma.rn(w[t], x[p + t], acc) for t ascending; the extra zero-tap terms at the two ends
+// add +0 to an accumulator that is +0 or positive, so with finite inputs (counts) the
+// result is bit-identical to fir_line4, with (NT + 1) x P/2 FFMA2 instead of NT x P FFMA.
+template <int R, int P, typename Load4, typename Store4>
+__device__ __forceinline__ void fir_line4_x2(int n, Load4 line4, Store4 store4) {
+    static_assert(P % 4 == 0, "P: whole float4 groups of outputs");
+    constexpr int NT = 2 * R + 1;
+    constexpr int NQ = P + NT - 1;
+    constexpr int NQ4 = (NQ + 3) / 4;
+    constexpr int M = P / 2;
+    for (int p0 = 0; p0 < n; p0 += P) {
+        uint64_t acc[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = 0ull;
+#pragma unroll
+        for (int q4 = 0; q4 < NQ4; ++q4) {
+            const float4 v4 = line4((p0 >> 2) + q4);
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = 4 * q4 + e;
+                uint64_t xx;
+                asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(vv[e]));
+#pragma unroll
+                for (int m = 0; m < M; ++m) {
+                    const int t = i - 2 * m;
+                    if (i < NQ && t >= 0 && t <= NT) {
+                        const uint64_t w2 = TapsOf<R / 3>::spair(t);
+                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc[m]) : "l"(w2), "l"(xx));
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < M; m += 2) {
+            float4 o;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(acc[m]));
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(o.z), "=f"(o.w) : "l"(acc[m + 1]));
+            store4(p0 + 2 * m, o);
+        }
     }
 }
 
@@ -224,8 +274,10 @@ __device__ __forceinline__ void smooth_h_tile(const T* __restrict__ in, float* _
         const float* row = sh + lane * ld + c0;
         float* orow = so + lane * op + c0;
         if ((CW & 15) == 0) {  // 16-byte reads of the row and 16-byte stores of the outputs
-            fir_line4<R, 16>(CW, [&](int q4) { return *reinterpret_cast<const float4*>(row + 4 * q4); },
-                             [&](int p, float4 v) { *reinterpret_cast<float4*>(orow + p) = v; });
+            auto ld4 = [&](int q4) { return *reinterpret_cast<const float4*>(row + 4 * q4); };
+            auto st4 = [&](int p, float4 v) { *reinterpret_cast<float4*>(orow + p) = v; };
+            if (INIM_FFMA2_H && CNT) fir_line4_x2<R, 16>(CW, ld4, st4);  // counts: finite
+            else fir_line4<R, 16>(CW, ld4, st4);
         } else {
             fir_line<R, 16>(taps, CW, [&](int q) { return row[q]; }, [&](int p, float v) { orow[p] = v; });
         }

@@ -158,16 +158,22 @@ int launch_smooth_state(const void* in, int in_kind, const Geo& g, const Ws& ws,
                               st, bt);
     Taps taps;
     make_taps(kernel_size, &taps);
-    const int emit = emit_aggregates ? 1 : 0;
+    static const bool fuse = [] {
+        const char* e = getenv("INIM_V_EMIT");
+        return !(e && e[0] == '0');
+    }();
+    const int emit = emit_aggregates && fuse ? 1 : 0;
+    int rc = INIM_EKERNEL;
     switch (kernel_size) {
 #define INIM_KS(K) \
-    case K: return launch_pair<K>(in, in_kind, g, ws, taps, background, d, emit, state, zero_next, st, bt);
+    case K: rc = launch_pair<K>(in, in_kind, g, ws, taps, background, d, emit, state, zero_next, st, bt); break;
         INIM_KS(1) INIM_KS(2) INIM_KS(3) INIM_KS(4) INIM_KS(5) INIM_KS(6) INIM_KS(7) INIM_KS(8)
         INIM_KS(9) INIM_KS(10) INIM_KS(11) INIM_KS(12) INIM_KS(13) INIM_KS(14) INIM_KS(15) INIM_KS(16)
 #undef INIM_KS
         default: break;
     }
-    return INIM_EKERNEL;
+    if (rc || !emit_aggregates || emit) return rc;
+    return launch_reduce_from_global(d, g, ws, nullptr, st, bt);
 }
 
 }  // namespace inim
