@@ -2,6 +2,7 @@
 // model.py:189-198) and the bilinear move (mapping.py:207-246 + the clip of
 // regularize.py:36).  Both stream the (n, 2) interleaved positions with 16-byte
 // vector accesses (two points per float4) and touch the grid through L2.
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -95,6 +96,108 @@ __device__ __forceinline__ void move_point(const float* tg, int s, float x, floa
     else bilinear<float>(reinterpret_cast<const float2*>(tg), s, x, y, ox, oy);
 }
 
+// Move of U point pairs per thread (pair u at index q[u], valid when ok[u]) and the
+// fused splat of the next iteration: shared by the grid-stride move and the pipelined
+// batch move.  Returns the thread's largest displacement.
+template <bool PAIRS, int U>
+__device__ __forceinline__ float move_pairs(const float* tg, int s, const float4 (&v)[U], const int64_t (&q)[U],
+                                            const bool (&ok)[U], float4* __restrict__ out2, int clip, bool stopped,
+                                            uint32_t* __restrict__ splat_next, int agg) {
+    float4 o[U];
+    float md = 0.f;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (stopped) {
+            o[u] = v[u];  // keep the ping-pong buffers consistent after a displacement stop
+            continue;
+        }
+        move_point<PAIRS>(tg, s, v[u].x, v[u].y, o[u].x, o[u].y);
+        move_point<PAIRS>(tg, s, v[u].z, v[u].w, o[u].z, o[u].w);
+        if (clip) {
+            o[u].x = clip01(o[u].x); o[u].y = clip01(o[u].y); o[u].z = clip01(o[u].z); o[u].w = clip01(o[u].w);
+        }
+        if (ok[u])
+            md = fmaxf(md, fmaxf(fmaxf(fabsf(o[u].x - v[u].x), fabsf(o[u].y - v[u].y)),
+                                 fmaxf(fabsf(o[u].z - v[u].z), fabsf(o[u].w - v[u].w))));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (ok[u]) __stcs(out2 + q[u], o[u]);
+    if (splat_next && !stopped) {
+        if (agg == 2) {
+            // float counts (exact integers below 2^24): lanes whose points fall in the
+            // same aligned group of four pixels merge into ONE 16-byte reduction
+            // (red.global.add.v4.f32), so the L2 sees a request per group, not per
+            // point (the splat's bound is the L2 reduction request rate)
+            const unsigned am = __activemask();
+            const int lane = threadIdx.x & 31;
+            float* fc = reinterpret_cast<float*>(splat_next);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pix = ok[u] ? pixel_of(h ? o[u].w : o[u].y, s) * s + pixel_of(h ? o[u].z : o[u].x, s)
+                                          : -1;
+                    const int g4 = pix >> 2;  // -1 for padding lanes
+                    const unsigned grp = __match_any_sync(am, g4);
+                    const int sub = pix & 3;
+                    const unsigned b1 = __ballot_sync(am, ok[u] && sub == 1);
+                    const unsigned b2 = __ballot_sync(am, ok[u] && sub == 2);
+                    const unsigned b3 = __ballot_sync(am, ok[u] && sub == 3);
+                    if (ok[u] && lane == __ffs(grp) - 1) {
+                        const int c1 = __popc(grp & b1), c2 = __popc(grp & b2), c3 = __popc(grp & b3);
+                        red_add_v4(fc + 4 * (int64_t)g4, (float)(__popc(grp) - c1 - c2 - c3), (float)c1,
+                                   (float)c2, (float)c3);
+                    }
+                }
+            }
+        } else if (agg) {  // points in pixel order: lanes sharing a pixel merge into one red.add
+            const unsigned am = __activemask();
+            const int lane = threadIdx.x & 31;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pix = ok[u] ? pixel_of(h ? o[u].w : o[u].y, s) * s + pixel_of(h ? o[u].z : o[u].x, s)
+                                          : -1;
+                    const unsigned grp = __match_any_sync(am, pix);
+                    if (ok[u] && lane == __ffs(grp) - 1) atomicAdd(splat_next + pix, (uint32_t)__popc(grp));
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (ok[u]) {
+                    atomicAdd(splat_next + pixel_of(o[u].y, s) * s + pixel_of(o[u].x, s), 1u);
+                    atomicAdd(splat_next + pixel_of(o[u].w, s) * s + pixel_of(o[u].z, s), 1u);
+                }
+            }
+        }
+    }
+    return md;
+}
+
+// The last point of an odd n (one thread).
+template <bool PAIRS>
+__device__ __forceinline__ float move_odd_tail(const float* tg, int s, const float* in, float* out, int64_t n, int clip,
+                                               bool stopped, uint32_t* splat_next, int agg) {
+    const float x = in[2 * (n - 1)], y = in[2 * (n - 1) + 1];
+    float ox = x, oy = y, md = 0.f;
+    if (!stopped) {
+        move_point<PAIRS>(tg, s, x, y, ox, oy);
+        if (clip) { ox = clip01(ox); oy = clip01(oy); }
+        md = fmaxf(fabsf(ox - x), fabsf(oy - y));
+    }
+    out[2 * (n - 1)] = ox;
+    out[2 * (n - 1) + 1] = oy;
+    if (splat_next && !stopped) {
+        const int pix = pixel_of(oy, s) * s + pixel_of(ox, s);
+        if (agg == 2) atomicAdd(reinterpret_cast<float*>(splat_next) + pix, 1.f);
+        else atomicAdd(splat_next + pix, 1u);
+    }
+    return md;
+}
+
 // BATCH: plot offsets of a SPLOM batch (grid.z), a separate instantiation so the
 // single-plot move keeps its register budget.
 template <bool PAIRS, int U, bool BATCH>
@@ -131,103 +234,106 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
     float md = 0.f;
     // U pairs of points (U 16-byte loads) per thread per step, all gathers in flight
     for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < npair; p0 += U * stride) {
-        float4 v[U], o[U];
+        float4 v[U];
+        int64_t q[U];
+        bool ok[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t q = p0 + u * stride;
-            v[u] = q < npair ? __ldcs(in2 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            q[u] = p0 + u * stride;
+            ok[u] = q[u] < npair;
+            v[u] = ok[u] ? __ldcs(in2 + q[u]) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (stopped) {
-                o[u] = v[u];  // keep the ping-pong buffers consistent after a displacement stop
-                continue;
-            }
-            move_point<PAIRS>(tg, s, v[u].x, v[u].y, o[u].x, o[u].y);
-            move_point<PAIRS>(tg, s, v[u].z, v[u].w, o[u].z, o[u].w);
-            if (clip) {
-                o[u].x = clip01(o[u].x); o[u].y = clip01(o[u].y); o[u].z = clip01(o[u].z); o[u].w = clip01(o[u].w);
-            }
-            if (p0 + u * stride < npair)
-                md = fmaxf(md, fmaxf(fmaxf(fabsf(o[u].x - v[u].x), fabsf(o[u].y - v[u].y)),
-                                     fmaxf(fabsf(o[u].z - v[u].z), fabsf(o[u].w - v[u].w))));
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (p0 + u * stride < npair) __stcs(out2 + p0 + u * stride, o[u]);
-        if (splat_next && !stopped) {
-            if (agg == 2) {
-                // float counts (exact integers below 2^24): lanes whose points fall in the
-                // same aligned group of four pixels merge into ONE 16-byte reduction
-                // (red.global.add.v4.f32), so the L2 sees a request per group, not per
-                // point (the splat's bound is the L2 reduction request rate)
-                const unsigned am = __activemask();
-                const int lane = threadIdx.x & 31;
-                float* fc = reinterpret_cast<float*>(splat_next);
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const bool ok = p0 + u * stride < npair;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int pix = ok ? pixel_of(h ? o[u].w : o[u].y, s) * s + pixel_of(h ? o[u].z : o[u].x, s)
-                                           : -1;
-                        const int g4 = pix >> 2;  // -1 for padding lanes
-                        const unsigned grp = __match_any_sync(am, g4);
-                        const int sub = pix & 3;
-                        const unsigned b1 = __ballot_sync(am, ok && sub == 1);
-                        const unsigned b2 = __ballot_sync(am, ok && sub == 2);
-                        const unsigned b3 = __ballot_sync(am, ok && sub == 3);
-                        if (ok && lane == __ffs(grp) - 1) {
-                            const int c1 = __popc(grp & b1), c2 = __popc(grp & b2), c3 = __popc(grp & b3);
-                            red_add_v4(fc + 4 * (int64_t)g4, (float)(__popc(grp) - c1 - c2 - c3), (float)c1,
-                                       (float)c2, (float)c3);
-                        }
-                    }
-                }
-            } else if (agg) {  // points in pixel order: lanes sharing a pixel merge into one red.add
-                const unsigned am = __activemask();
-                const int lane = threadIdx.x & 31;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const bool ok = p0 + u * stride < npair;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int pix = ok ? pixel_of(h ? o[u].w : o[u].y, s) * s + pixel_of(h ? o[u].z : o[u].x, s)
-                                           : -1;
-                        const unsigned grp = __match_any_sync(am, pix);
-                        if (ok && lane == __ffs(grp) - 1) atomicAdd(splat_next + pix, (uint32_t)__popc(grp));
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (p0 + u * stride < npair) {
-                        atomicAdd(splat_next + pixel_of(o[u].y, s) * s + pixel_of(o[u].x, s), 1u);
-                        atomicAdd(splat_next + pixel_of(o[u].w, s) * s + pixel_of(o[u].z, s), 1u);
-                    }
-                }
-            }
-        }
+        md = fmaxf(md, move_pairs<PAIRS, U>(tg, s, v, q, ok, out2, clip, stopped, splat_next, agg));
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const float x = in[2 * (n - 1)], y = in[2 * (n - 1) + 1];
-        float ox = x, oy = y;
-        if (!stopped) {
-            move_point<PAIRS>(tg, s, x, y, ox, oy);
-            if (clip) { ox = clip01(ox); oy = clip01(oy); }
-            md = fmaxf(md, fmaxf(fabsf(ox - x), fabsf(oy - y)));
-        }
-        out[2 * (n - 1)] = ox;
-        out[2 * (n - 1) + 1] = oy;
-        if (splat_next && !stopped) {
-            const int pix = pixel_of(oy, s) * s + pixel_of(ox, s);
-            if (agg == 2) atomicAdd(reinterpret_cast<float*>(splat_next) + pix, 1.f);
-            else atomicAdd(splat_next + pix, 1u);
-        }
-    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+        md = fmaxf(md, move_odd_tail<PAIRS>(tg, s, in, out, n, clip, stopped, splat_next, agg));
     if (max_disp && !stopped) {
         md = warp_max(md);
         if ((threadIdx.x & 31) == 0 && md > 0.f) atomic_max_nonneg(max_disp, md);
+    }
+}
+
+// Batch move with the point pairs staged by bulk copies: each CTA walks chunks of
+// kMoveChunk pairs of its plot (grid.x CTAs per plot, grid-stride), and one thread
+// issues the cp.async.bulk of chunk i + 1 into the other half of a two-slot shared
+// buffer before the CTA works on chunk i, so the positions' HBM latency overlaps the
+// previous chunk's gathers (the grid-stride move exposes it once per thread).  Same
+// per-point arithmetic and splat as sample_f32_kernel: bit-identical results.
+constexpr int kMoveU = 4;
+constexpr int kMoveChunk = 256 * kMoveU;  // pairs per chunk (16 KB)
+
+template <bool PAIRS>
+__global__ void __launch_bounds__(256) move_bulk_kernel(const float* __restrict__ tg, int k,
+                                                        const float* __restrict__ in, float* __restrict__ out,
+                                                        int64_t n, int clip, float* max_disp, const int* state,
+                                                        uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
+                                                        int agg, int64_t zin, int64_t zout, int64_t zslab) {
+    __shared__ __align__(128) float4 buf[2][kMoveChunk];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int64_t zo = zslab_off(zslab);
+    tg = zoff(tg, zo);
+    in += blockIdx.z * zin;
+    out += blockIdx.z * zout;
+    max_disp = zoff_opt(max_disp, zo);
+    splat_next = zoff_opt(splat_next, zo);
+    zn0 = zoff_opt(zn0, zo);
+    zn1 = zoff_opt(zn1, zo);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_enter();
+    state = zstate(state, zslab);
+    const bool stopped = state && state[0];
+    const int s = 1 << k;
+    if (splat_next && !stopped && blockIdx.x == 0 && tid == 0) {
+        if (zn0) *zn0 = 0.f;
+        if (zn1) *zn1 = 0.f;
+    }
+    const int64_t npair = n >> 1;
+    const int64_t nchunk = (npair + kMoveChunk - 1) / kMoveChunk;
+    const float4* in2 = reinterpret_cast<const float4*>(in);
+    float4* out2 = reinterpret_cast<float4*>(out);
+    auto issue = [&](int64_t c, int slot) {  // one thread: chunk c -> buf[slot]
+        const int64_t p = c * kMoveChunk;
+        const int64_t cnt = npair - p < kMoveChunk ? npair - p : kMoveChunk;
+        const uint32_t bytes = (uint32_t)(cnt * 16);
+        fence_proxy_async();  // the slot's previous contents were read by the generic proxy
+        mbar_arrive_expect_tx(&bar[slot], bytes);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(&buf[slot][0])),
+                     "l"(reinterpret_cast<uint64_t>(in2 + p)), "r"(bytes), "r"(smem_u32(&bar[slot]))
+                     : "memory");
+    };
+    float md = 0.f;
+    int64_t c = blockIdx.x;
+    if (tid == 0 && c < nchunk) issue(c, 0);
+    for (int i = 0; c < nchunk; ++i, c += gridDim.x) {
+        const int slot = i & 1;
+        if (tid == 0 && c + gridDim.x < nchunk) issue(c + gridDim.x, slot ^ 1);
+        mbar_wait(&bar[slot], (uint32_t)((i >> 1) & 1));
+        const int64_t p = c * kMoveChunk;
+        float4 v[kMoveU];
+        int64_t q[kMoveU];
+        bool ok[kMoveU];
+#pragma unroll
+        for (int u = 0; u < kMoveU; ++u) {
+            const int e = u * 256 + tid;
+            q[u] = p + e;
+            ok[u] = q[u] < npair;
+            v[u] = ok[u] ? buf[slot][e] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        md = fmaxf(md, move_pairs<PAIRS, kMoveU>(tg, s, v, q, ok, out2, clip, stopped, splat_next, agg));
+        __syncthreads();  // buf[slot] is refilled two chunks later
+    }
+    if ((n & 1) && blockIdx.x == 0 && tid == 0)
+        md = fmaxf(md, move_odd_tail<PAIRS>(tg, s, in, out, n, clip, stopped, splat_next, agg));
+    if (max_disp && !stopped) {
+        md = warp_max(md);
+        if ((tid & 31) == 0 && md > 0.f) atomic_max_nonneg(max_disp, md);
     }
 }
 
@@ -545,6 +651,26 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
     // 346.6 us), four in a batch (C4: 50.4 vs 55.0 ms)
     // a batch (HBM-latency bound, work for many waves): UB point pairs per thread
     constexpr int UB = INIM_BATCH_MOVE_U;
+    static const int bulk_cpc = [] {  // chunks per CTA of the pipelined batch move (0: grid-stride move)
+        const char* e = getenv("INIM_MOVE_BULK");
+        return e ? atoi(e) : 4;
+    }();
+    static const int64_t bulk_single = [] {  // single plots: pipelined move from this many pairs on
+        const char* e = getenv("INIM_MOVE_BULK_SINGLE");
+        return e ? (int64_t)atoll(e) : (int64_t)-1;
+    }();
+    if (bulk_cpc > 0 && (n >> 1) > 0 && (bt.B > 1 || (bulk_single >= 0 && (n >> 1) >= bulk_single))) {
+        auto kb = pairs ? move_bulk_kernel<true> : move_bulk_kernel<false>;
+        // many CTAs of a few chunks each: the prefetch overlaps all but the first chunk's
+        // load, and the grid is many waves deep (no tail)
+        const int64_t nchunk = ((n >> 1) + kMoveChunk - 1) / kMoveChunk;
+        const int64_t per_plot = (nchunk + bulk_cpc - 1) / bulk_cpc;
+        INIM_CUDA_TRY(launch_pdl(kb, dim3((unsigned)per_plot, 1, (unsigned)bt.B), dim3(256), 0, st, tg, k, in, out, n,
+                                 clip, max_disp, state, splat_next, zn0, zn1, sorted ? (f32_counts ? 2 : 1) : 0, zin,
+                                 zout, bt.slab));
+        prof_mark(st, "sample");
+        return (int)cudaGetLastError();
+    }
     auto kern = bt.B > 1 ? (pairs ? sample_f32_kernel<true, UB, true> : sample_f32_kernel<false, UB, true>)
                          : (pairs ? sample_f32_kernel<true, 2, false> : sample_f32_kernel<false, 1, false>);
     const dim3 grid = batch_grid(resident_grid((const void*)kern, npair > 0 ? npair : 1, 256), npair,
