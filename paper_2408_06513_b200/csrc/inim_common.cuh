@@ -114,6 +114,15 @@ INIM_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, int x, int y, 
         : "memory");
 }
 
+// 16-byte asynchronous global -> shared copy through L2 (cp.async.cg) and its wait.
+INIM_DEV void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+
+INIM_DEV void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 INIM_DEV void prefetch_tensormap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

@@ -10,6 +10,9 @@
 #ifndef INIM_FFMA2_V
 #define INIM_FFMA2_V 1  // vertical pass on packed fma.rn.f32x2 (0: scalar FFMA immediates)
 #endif
+#ifndef INIM_V_CPASYNC
+#define INIM_V_CPASYNC 1  // vertical staging by cp.async (0: register-staged loads, four rows in flight)
+#endif
 #ifndef INIM_FFMA2_H
 #define INIM_FFMA2_H 1  // horizontal pass on packed fma.rn.f32x2 (0: scalar FFMA immediates)
 #endif
@@ -408,7 +411,23 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     const int a0 = by * VR, i0 = x * TW;
     const int H = VR + 2 * R;
     const bool interior = a0 - R >= 0 && a0 + VR + R <= s;
-    if ((TW & 3) == 0) {
+    if ((TW & 3) == 0 && INIM_V_CPASYNC) {
+        // (TW/4) float4 per row: every 16-byte piece of the staging tile is requested at
+        // once as an asynchronous global -> shared copy (cp.async.cg, no register
+        // staging), so the tile costs one memory round trip
+        const int TW4 = TW >> 2;
+        const int cpr = TW4 < (int)blockDim.x ? TW4 : (int)blockDim.x;  // threads per row
+        const int rpp = blockDim.x / cpr;                                // rows per pass
+        const int c4 = threadIdx.x % cpr;
+        if (c4 < TW4) {
+            for (int r = threadIdx.x / cpr; r < H; r += rpp) {
+                const int row = interior ? a0 - R + r : reflect_index(a0 - R + r, s);
+                cp_async16(reinterpret_cast<float4*>(sh) + r * TW4 + c4,
+                           reinterpret_cast<const float4*>(tmp + (int64_t)row * s + i0) + c4);
+            }
+        }
+        cp_async_wait_all();
+    } else if ((TW & 3) == 0) {
         // (TW/4) float4 per row; threads tile (rows x float4 columns) without division
         const int TW4 = TW >> 2;
         const int cpr = TW4 < (int)blockDim.x ? TW4 : (int)blockDim.x;  // threads per row
