@@ -135,6 +135,15 @@ int inim_flat_response_f64(int k, double* defect, cudaStream_t stream);
 int inim_cast_f64_to_f32(const double* in, float* out, int64_t count, cudaStream_t stream);
 int inim_cast_f32_to_f64(const float* in, double* out, int64_t count, cudaStream_t stream);
 
+/* Host float64 <-> device float32 transfers for pageable host buffers (the mirror's
+ * to_device / to_host of the reference's float64 position arrays): the host narrows or
+ * widens 1 MiB chunks with its cores while the DMA engine moves the previous one through
+ * two page-locked slots.  h2d returns once the last chunk is queued on `stream` (the host
+ * buffer may be reused immediately); d2h returns with `host` complete.  Same IEEE
+ * round-to-nearest conversion as inim_cast_*. */
+int inim_h2d_narrow(const double* host, float* dev, int64_t count, cudaStream_t stream);
+int inim_d2h_widen(const float* dev, double* host, int64_t count, cudaStream_t stream);
+
 /* One iteration of regularize.iterate_once (regularize.py:25-37), device resident:
  * counts <- 0; splat(pts_in); smooth (+background); integral+field; sample+clip into
  * pts_out.  counts: s*s uint32; d: s*s float; targets: s*s*2 float.  background <= 0

@@ -50,6 +50,8 @@ _SIGS = {
     "inim_tilted_wedges": (c_int, [c_void_p] * 6 + [c_int, c_void_p, c_void_p, c_void_p]),
     "inim_cast_f64_to_f32": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "inim_cast_f32_to_f64": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
+    "inim_h2d_narrow": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
+    "inim_d2h_widen": (c_int, [c_void_p, c_void_p, c_i64, c_void_p]),
     "inim_iterate": (c_int, [c_void_p, c_void_p, c_i64, c_int, c_int, c_float, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p, c_void_p]),
     "inim_run": (c_int, [c_void_p, c_i64, c_int, c_int, c_float, c_int, c_float, c_void_p, c_void_p, c_void_p,

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 #include "inim_internal.cuh"
 
 namespace inim {
@@ -367,6 +369,48 @@ static int enqueue_run(const RunKey& key, float* pts, float* frames, float* fiel
 
 using namespace inim;
 
+// ------------------------------------------------------------ host <-> device staging
+// Pipelined host transfers for host (pageable) float64 buffers: the host narrows /
+// widens chunks in parallel (OpenMP) through two page-locked float32 slots while the
+// DMA engine moves the other slot, so the copy runs at page-locked PCIe speed on half
+// the bytes instead of a single-threaded pageable float64 copy.  float64 <-> float32 on
+// the host is the same IEEE round-to-nearest conversion as the device cast kernels.
+namespace {
+constexpr int64_t kStageChunk = int64_t(1) << 18;  // floats per slot (1 MiB)
+
+struct Staging {
+    std::mutex mu;
+    float* slot[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    int dev = -1;
+};
+Staging g_stage;
+
+int staging_ready(Staging& S) {
+    int dev = 0;
+    INIM_CUDA_TRY(cudaGetDevice(&dev));
+    if (S.slot[0] && S.dev == dev) return 0;
+    for (int q = 0; q < 2; ++q) {
+        if (S.slot[q]) {
+            cudaFreeHost(S.slot[q]);
+            cudaEventDestroy(S.done[q]);
+        }
+        INIM_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&S.slot[q]), kStageChunk * sizeof(float),
+                                    cudaHostAllocDefault));
+        INIM_CUDA_TRY(cudaEventCreateWithFlags(&S.done[q], cudaEventDisableTiming));
+        INIM_CUDA_TRY(cudaEventRecord(S.done[q], 0));
+    }
+    S.dev = dev;
+    return 0;
+}
+
+int stage_threads(int64_t count) {
+    const int t = omp_get_max_threads();
+    const int cap = count >= (int64_t(1) << 16) ? 16 : 1;
+    return t < cap ? t : cap;
+}
+}  // namespace
+
 extern "C" {
 
 const char* inim_version(void) { return "libinim sm_100a 0.1"; }
@@ -486,6 +530,59 @@ int inim_cast_f64_to_f32(const double* in, float* out, int64_t count, cudaStream
     if (count < 0 || (count > 0 && (!in || !out))) return INIM_EINVAL;
     if (count == 0) return 0;
     return launch_cast_f64_f32(in, out, count, stream);
+}
+
+int inim_h2d_narrow(const double* host, float* dev, int64_t count, cudaStream_t stream) {
+    if (count < 0 || (count > 0 && (!host || !dev))) return INIM_EINVAL;
+    if (count == 0) return 0;
+    std::lock_guard<std::mutex> lock(g_stage.mu);
+    int rc = staging_ready(g_stage);
+    if (rc) return rc;
+    const int nt = stage_threads(count);
+    for (int64_t off = 0, c = 0; off < count; off += kStageChunk, ++c) {
+        const int q = (int)(c & 1);
+        const int64_t len = count - off < kStageChunk ? count - off : kStageChunk;
+        INIM_CUDA_TRY(cudaEventSynchronize(g_stage.done[q]));  // the slot's previous DMA has finished
+        float* dst = g_stage.slot[q];
+        const double* src = host + off;
+#pragma omp parallel for num_threads(nt) schedule(static)
+        for (int64_t i = 0; i < len; ++i) dst[i] = (float)src[i];
+        INIM_CUDA_TRY(cudaMemcpyAsync(dev + off, dst, len * sizeof(float), cudaMemcpyHostToDevice, stream));
+        INIM_CUDA_TRY(cudaEventRecord(g_stage.done[q], stream));
+    }
+    return 0;
+}
+
+int inim_d2h_widen(const float* dev, double* host, int64_t count, cudaStream_t stream) {
+    if (count < 0 || (count > 0 && (!host || !dev))) return INIM_EINVAL;
+    if (count == 0) return 0;
+    std::lock_guard<std::mutex> lock(g_stage.mu);
+    int rc = staging_ready(g_stage);
+    if (rc) return rc;
+    const int nt = stage_threads(count);
+    const int64_t nchunk = (count + kStageChunk - 1) / kStageChunk;
+    auto issue = [&](int64_t c) -> int {  // DMA chunk c into its slot
+        const int q = (int)(c & 1);
+        const int64_t off = c * kStageChunk;
+        const int64_t len = count - off < kStageChunk ? count - off : kStageChunk;
+        INIM_CUDA_TRY(cudaMemcpyAsync(g_stage.slot[q], dev + off, len * sizeof(float), cudaMemcpyDeviceToHost,
+                                      stream));
+        INIM_CUDA_TRY(cudaEventRecord(g_stage.done[q], stream));
+        return 0;
+    };
+    if ((rc = issue(0))) return rc;
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int q = (int)(c & 1);
+        INIM_CUDA_TRY(cudaEventSynchronize(g_stage.done[q]));
+        if (c + 1 < nchunk && (rc = issue(c + 1))) return rc;  // the other slot was widened last step
+        const int64_t off = c * kStageChunk;
+        const int64_t len = count - off < kStageChunk ? count - off : kStageChunk;
+        const float* src = g_stage.slot[q];
+        double* dst = host + off;
+#pragma omp parallel for num_threads(nt) schedule(static)
+        for (int64_t i = 0; i < len; ++i) dst[i] = (double)src[i];
+    }
+    return 0;
 }
 
 int inim_cast_f32_to_f64(const float* in, double* out, int64_t count, cudaStream_t stream) {
@@ -724,18 +821,16 @@ int inim_run_host(const double* pts_host, double* out_host, int64_t n, int k, in
         cap = n;
         inim_clear_graph_cache();
     }
-    if (n > 0) {
-        INIM_CUDA_TRY(cudaMemcpyAsync(pd, pts_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
-        int rc = launch_cast_f64_f32(pd, pf, 2 * n, st);
+    if (n > 0) {  // narrowed on the host while the DMA runs (page-locked float32 slots)
+        int rc = inim_h2d_narrow(pts_host, pf, 2 * n, st);
         if (rc) return rc;
     }
     int rc = inim_run(pf, n, k, kernel_size, (float)background, iterations, 0.f, nullptr, nullptr, nullptr, nullptr,
                       nullptr, ws, st);
     if (rc) return rc;
     if (n > 0) {
-        rc = launch_cast_f32_f64(pf, pd, 2 * n, st);
+        rc = inim_d2h_widen(pf, out_host, 2 * n, st);
         if (rc) return rc;
-        INIM_CUDA_TRY(cudaMemcpyAsync(out_host, pd, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, st));
     }
     INIM_CUDA_TRY(cudaStreamSynchronize(st));
     return 0;
