@@ -254,13 +254,17 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
 }
 
 // Batch move with the point pairs staged by bulk copies: each CTA walks chunks of
-// kMoveChunk pairs of its plot (grid.x CTAs per plot, grid-stride), and one thread
+// kMoveChunk pairs of its plot (grid.x CTAs per plot, grid-stride; two pairs per thread
+// per chunk and eight chunks per CTA measured best), and one thread
 // issues the cp.async.bulk of chunk i + 1 into the other half of a two-slot shared
 // buffer before the CTA works on chunk i, so the positions' HBM latency overlaps the
 // previous chunk's gathers (the grid-stride move exposes it once per thread).  Same
 // per-point arithmetic and splat as sample_f32_kernel: bit-identical results.
-constexpr int kMoveU = 4;
-constexpr int kMoveChunk = 256 * kMoveU;  // pairs per chunk (16 KB)
+#ifndef INIM_BULK_U
+#define INIM_BULK_U 2
+#endif
+constexpr int kMoveU = INIM_BULK_U;
+constexpr int kMoveChunk = 256 * kMoveU;  // pairs per chunk (8 KB)
 
 template <bool PAIRS>
 __global__ void __launch_bounds__(256) move_bulk_kernel(const float* __restrict__ tg, int k,
@@ -653,7 +657,7 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
     constexpr int UB = INIM_BATCH_MOVE_U;
     static const int bulk_cpc = [] {  // chunks per CTA of the pipelined batch move (0: grid-stride move)
         const char* e = getenv("INIM_MOVE_BULK");
-        return e ? atoi(e) : 4;
+        return e ? atoi(e) : 8;
     }();
     static const int64_t bulk_single = [] {  // single plots: pipelined move from this many pairs on
         const char* e = getenv("INIM_MOVE_BULK_SINGLE");
