@@ -57,6 +57,47 @@ __device__ __forceinline__ void bilinear_pairs(const float4* __restrict__ tp, in
     oy = w00 * r0.y + w10 * r0.w + w01 * r1.y + w11 * r1.w;
 }
 
+// The float32 bilinear sample split into its gathers and its blend, so a caller can put
+// the gathers of several points in flight before the first blend (same values and
+// arithmetic as bilinear / bilinear_pairs).
+struct Tap4 {
+    float4 r0, r1;  // (t00, t10) and (t01, t11) as (x, y, x, y)
+    float fx, fy;
+};
+
+template <bool PAIRS>
+__device__ __forceinline__ Tap4 bilinear_fetch(const float* tg, int s, float x, float y) {
+    const float sx = x * (float)s, sy = y * (float)s;
+    int i0 = (int)floorf(sx), j0 = (int)floorf(sy);
+    i0 = i0 < 0 ? 0 : (i0 > s - 2 ? s - 2 : i0);
+    j0 = j0 < 0 ? 0 : (j0 > s - 2 ? s - 2 : j0);
+    Tap4 t;
+    t.fx = sx - (float)i0;
+    t.fy = sy - (float)j0;
+    const int64_t base = (int64_t)j0 * s + i0;
+    if (PAIRS) {
+        const float4* tp = reinterpret_cast<const float4*>(tg);
+        t.r0 = __ldg(tp + base);
+        t.r1 = __ldg(tp + base + s);
+    } else {
+        const float2* tp = reinterpret_cast<const float2*>(tg);
+        const float2 a = __ldg(tp + base), b = __ldg(tp + base + 1);
+        const float2 c = __ldg(tp + base + s), d = __ldg(tp + base + s + 1);
+        t.r0 = make_float4(a.x, a.y, b.x, b.y);
+        t.r1 = make_float4(c.x, c.y, d.x, d.y);
+    }
+    return t;
+}
+
+__device__ __forceinline__ void bilinear_blend(const Tap4& t, float& ox, float& oy) {
+    const float w00 = (1.f - t.fx) * (1.f - t.fy);
+    const float w10 = t.fx * (1.f - t.fy);
+    const float w01 = (1.f - t.fx) * t.fy;
+    const float w11 = t.fx * t.fy;
+    ox = w00 * t.r0.x + w10 * t.r0.z + w01 * t.r1.x + w11 * t.r1.z;
+    oy = w00 * t.r0.y + w10 * t.r0.w + w01 * t.r1.y + w11 * t.r1.w;
+}
+
 template <typename T>
 __device__ __forceinline__ T clip01(T v) {
     return v < (T)0 ? (T)0 : (v > (T)1 ? (T)1 : v);

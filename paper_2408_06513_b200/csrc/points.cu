@@ -99,20 +99,36 @@ __device__ __forceinline__ void move_point(const float* tg, int s, float x, floa
 // Move of U point pairs per thread (pair u at index q[u], valid when ok[u]) and the
 // fused splat of the next iteration: shared by the grid-stride move and the pipelined
 // batch move.  Returns the thread's largest displacement.
-template <bool PAIRS, int U>
+template <bool PAIRS, int U, bool GATHER_FIRST = false>
 __device__ __forceinline__ float move_pairs(const float* tg, int s, const float4 (&v)[U], const int64_t (&q)[U],
                                             const bool (&ok)[U], float4* __restrict__ out2, int clip, bool stopped,
                                             uint32_t* __restrict__ splat_next, int agg) {
     float4 o[U];
     float md = 0.f;
+    if (GATHER_FIRST && !stopped) {
+        // every gather of the thread's 2U points in flight before the first blend
+        Tap4 t[U][2];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            t[u][0] = bilinear_fetch<PAIRS>(tg, s, v[u].x, v[u].y);
+            t[u][1] = bilinear_fetch<PAIRS>(tg, s, v[u].z, v[u].w);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bilinear_blend(t[u][0], o[u].x, o[u].y);
+            bilinear_blend(t[u][1], o[u].z, o[u].w);
+        }
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (stopped) {
             o[u] = v[u];  // keep the ping-pong buffers consistent after a displacement stop
             continue;
         }
-        move_point<PAIRS>(tg, s, v[u].x, v[u].y, o[u].x, o[u].y);
-        move_point<PAIRS>(tg, s, v[u].z, v[u].w, o[u].z, o[u].w);
+        if (!GATHER_FIRST) {
+            move_point<PAIRS>(tg, s, v[u].x, v[u].y, o[u].x, o[u].y);
+            move_point<PAIRS>(tg, s, v[u].z, v[u].w, o[u].z, o[u].w);
+        }
         if (clip) {
             o[u].x = clip01(o[u].x); o[u].y = clip01(o[u].y); o[u].z = clip01(o[u].z); o[u].w = clip01(o[u].w);
         }
@@ -260,6 +276,9 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
 // buffer before the CTA works on chunk i, so the positions' HBM latency overlaps the
 // previous chunk's gathers (the grid-stride move exposes it once per thread).  Same
 // per-point arithmetic and splat as sample_f32_kernel: bit-identical results.
+#ifndef INIM_GATHER_FIRST
+#define INIM_GATHER_FIRST 1  // pipelined move: all gathers of a thread issued before the blends
+#endif
 #ifndef INIM_BULK_U
 #define INIM_BULK_U 2
 #endif
@@ -330,7 +349,8 @@ __global__ void __launch_bounds__(256) move_bulk_kernel(const float* __restrict_
             ok[u] = q[u] < npair;
             v[u] = ok[u] ? buf[slot][e] : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        md = fmaxf(md, move_pairs<PAIRS, kMoveU>(tg, s, v, q, ok, out2, clip, stopped, splat_next, agg));
+        md = fmaxf(md, move_pairs<PAIRS, kMoveU, INIM_GATHER_FIRST>(tg, s, v, q, ok, out2, clip, stopped, splat_next,
+                                                                     agg));
         __syncthreads();  // buf[slot] is refilled two chunks later
     }
     if ((n & 1) && blockIdx.x == 0 && tid == 0)
