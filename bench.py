@@ -154,7 +154,7 @@ def algorithmic_bytes(name: str, n: int, m: int) -> int:
 
 
 # ncu kernel names -> the names inim_profile_run reports
-NCU_NAMES = {"sample_f32_kernel": "sample", "write_kernel": "write_field", "smooth_h_kernel": "smooth_h",
+NCU_NAMES = {"sample_f32_kernel": "sample", "move_bulk_kernel": "sample", "write_kernel": "write_field", "smooth_h_kernel": "smooth_h",
              "smooth_v_kernel": "smooth_v_reduce", "chains_kernel": "chains", "splat_f32_kernel": "splat",
              "lines_kernel": "lines", "chains_reg_kernel": "chains"}
 

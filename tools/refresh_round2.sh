@@ -27,6 +27,6 @@ PROF_ITERS=3 ncu --set full --import-source on --clock-control none --metrics $A
     -k regex:"splat_f32|sample_f32|smooth|write_kernel|chains" --launch-skip 0 -c 8 \
     -o $O/full_iter_c3 python tools/prof_driver.py iter3 > $O/ncu_full_c3.log 2>&1
 PROF_PLOTS=32 PROF_ITERS=3 ncu --set full --import-source on --clock-control none \
-    -k regex:"sample_f32|write_kernel|smooth_v|smooth_h|chains" --launch-skip 10 -c 5 \
+    -k regex:"move_bulk|write_kernel|smooth_v|smooth_h|chains" --launch-skip 10 -c 5 \
     -o $O/full_splom python tools/prof_driver.py splom > $O/ncu_full_splom.log 2>&1
 ls -la $O
