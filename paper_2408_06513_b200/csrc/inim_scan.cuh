@@ -77,8 +77,8 @@ __host__ __device__ inline int chain_kind(const Geo& g, int item) {
     return item < ntl ? 0 : (item < ntl + chain_groups_x(g) ? 1 : 2);
 }
 // band chunks per chain (warps per CTA): short serial chunks on small grids
-__host__ __device__ inline int chain_warps(const Geo& g) {
-    const int ny = g.B / 4;
+__host__ __device__ inline int chain_warps(const Geo& g, int per = 4) {
+    const int ny = g.B / per;
     return ny < 1 ? 1 : (ny > 16 ? 16 : ny);
 }
 

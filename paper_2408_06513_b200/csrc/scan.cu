@@ -76,12 +76,25 @@ __global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws0, 
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st, const Bat& bt) {
     INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B, 1, bt.B), dim3(32 * g.TH), 0, st, g, ws, state, bt.slab));
     prof_mark(st, "lines");
-    const int ny = chain_warps(g), ch = (g.B + ny - 1) / ny;
+    const bool batch = bt.B > 1;
+    static const int batch_per = [] {  // INIM_CHAIN_PER: step terms per thread in a batch (4 or 8)
+        const char* e = getenv("INIM_CHAIN_PER");
+        const int v = e ? atoi(e) : 8;
+        return v == 16 ? 16 : (v == 4 ? 4 : 8);
+    }();
+    // one plot: 4 (C2 43.6 vs 45.0 us, C3 307.9 vs 309.3 us with 8); a batch: 8
+    const int per = batch ? batch_per : 4;
+    const int ny = chain_warps(g, per), ch = (g.B + ny - 1) / ny;
     const dim3 grid(chains_items(g), 1, bt.B), block(32 * ny);
+    if (batch && ch > 4 && ch <= 16) {
+        INIM_CUDA_TRY(launch_pdl(ch <= 8 ? chains_reg_kernel<8, true> : chains_reg_kernel<16, true>, grid, block, 0,
+                                 st, g, ws, state, bt.slab));
+        prof_mark(st, "chains");
+        return (int)cudaGetLastError();
+    }
     // register-held chunks pay off only while they are short (measured: 1024^2 +7% on
     // the integral sweep; 4096^2 +-0; 8192^2 and up -10%, occupancy); longer chunks run
     // the two-pass kernel
-    const bool batch = bt.B > 1;
     if (ch <= 4) {
         INIM_CUDA_TRY(launch_pdl(batch ? chains_reg_kernel<4, true> : chains_reg_kernel<4, false>, grid, block, 0, st,
                                  g, ws, state, bt.slab));
