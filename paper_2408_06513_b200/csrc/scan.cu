@@ -57,7 +57,21 @@ __global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws0, 
     __shared__ double rowtot[32];
     const int b = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int TH = g.TH, NX = g.NX, a = b * TH;
-    {
+    if (NX < 32) {
+        // 32 / NX rows per warp, one NX-lane segment each (the same adds, in the same
+        // order, as warp_line_prefix's full-warp scan, whose upper lanes hold zeros)
+        const int row = w * (32 / NX) + lane / NX, x = lane % NX;
+        if (row < TH) {
+            const double v = (double)__ldcg(ws.rowsum + (int64_t)(a + row) * NX + x);
+            double inc = v;
+            for (int d = 1; d < NX; d <<= 1) {
+                const double t = __shfl_up_sync(kFull, inc, d, NX);
+                if (x >= d) inc += t;
+            }
+            ws.hc[(int64_t)(a + row) * NX + x] = inc - v;
+            if (x == NX - 1) rowtot[row] = inc;
+        }
+    } else {
         const double t = warp_line_prefix(ws.rowsum + (int64_t)(a + w) * NX, ws.hc + (int64_t)(a + w) * NX, NX, lane);
         if (lane == 0) rowtot[w] = t;
     }
@@ -74,7 +88,11 @@ __global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws0, 
 }
 
 int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaStream_t st, const Bat& bt) {
-    INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B, 1, bt.B), dim3(32 * g.TH), 0, st, g, ws, state, bt.slab));
+    // one warp per row, or 32 / NX rows per warp on narrow grids (at least two warps: the
+    // band-total scan runs on warp 1)
+    int lt = g.NX < 32 ? (g.TH * g.NX + 31) / 32 * 32 : 32 * g.TH;
+    if (lt < 64) lt = 64;
+    INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B, 1, bt.B), dim3(lt), 0, st, g, ws, state, bt.slab));
     prof_mark(st, "lines");
     const bool batch = bt.B > 1;
     static const int batch_per = [] {  // INIM_CHAIN_PER: step terms per thread in a batch (4 or 8)
