@@ -31,6 +31,22 @@ def shard(nplots: int, world: int, rank: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+def _chunk_bounds(nb: int, chunk: int, lead: int) -> list:
+    """[b0, b1) plot ranges for run_host: `lead` plots first and last, the rest in
+    near-equal chunks of at most `chunk`."""
+    if lead <= 0 or nb <= 2 * lead + chunk:
+        sizes = [chunk] * (nb // chunk) + ([nb % chunk] if nb % chunk else [])
+    else:
+        mid = nb - 2 * lead
+        k = -(-mid // chunk)
+        sizes = [lead] + [mid // k + (1 if q < mid % k else 0) for q in range(k)] + [lead]
+    out, b0 = [], 0
+    for n in sizes:
+        out.append((b0, b0 + n))
+        b0 += n
+    return out
+
+
 def splom_plot(idx: int, n: int, seed: int = 2408) -> np.ndarray:
     """Synthetic plot `idx` of the batch: a Gaussian mixture of 1-8 clusters (PCG64
     stream seeded by (seed, idx), the reference suite's seeding pattern,
@@ -124,12 +140,13 @@ class DeviceSplom:
                 on_chunk(b0, b1)
         return self.work
 
-    def run_host(self, host_in, host_out, chunk: int = 64):
+    def run_host(self, host_in, host_out, chunk: int = 64, lead: int = 32):
         """The whole block from page-locked host buffers: (B, n, 2) float32 in, final
-        positions out.  The plots go in chunks of `chunk`: chunk c + 1 is copied in on
-        one copy stream and chunk c - 1 copied out on another while chunk c runs (the
+        positions out.  The plots go in chunks of about `chunk`: chunk c + 1 is copied in
+        on one copy stream and chunk c - 1 copied out on another while chunk c runs (the
         copy engines work beside the SMs), so the step costs about max(compute,
-        transfers) instead of their sum.  Returns host_out."""
+        transfers) instead of their sum.  The first and the last chunk hold only `lead`
+        plots: their copy in / out is the part nothing overlaps.  Returns host_out."""
         torch, D, lib, cfg = self.torch, self.D, self.lib, self.cfg
         nb = len(self.ids)
         chunk = max(1, min(chunk, self.batch))
@@ -140,7 +157,7 @@ class DeviceSplom:
         h2d.wait_event(start)
         d2h.wait_event(start)
         copied, ran = [], []
-        bounds = [(b0, min(b0 + chunk, nb)) for b0 in range(0, nb, chunk)]
+        bounds = _chunk_bounds(nb, chunk, min(lead, chunk))
         for b0, b1 in bounds:  # all copies in, in order, on their own stream
             with torch.cuda.stream(h2d):
                 self.work[b0:b1].copy_(host_in[b0:b1], non_blocking=True)
