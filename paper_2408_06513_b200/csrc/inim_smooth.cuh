@@ -402,7 +402,7 @@ __host__ __device__ inline size_t v_smem_bytes(const Geo& g, const VGeo& v, int 
 template <int R>
 __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, float* __restrict__ d, const Geo& g,
                                               const VGeo& v, const Ws& ws, const Taps& taps, float background,
-                                              int emit, int bx, int by, float* vsm) {
+                                              int emit, int bx, int by, float* vsm, uint32_t* zero_next = nullptr) {
     const int TH = g.TH, TW = g.TW, s = g.s, VR = v.VR;
     const bool inplace = v_inplace(TH, TW, v.GT);
     float* sh = vsm;                                                 // [(VR + 2R)][TW]
@@ -480,17 +480,23 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
             else warp_tile_reduce<1>(src, TW, g, ws, b, x, lane);
         }
     }
-    // the VR x TW tile of d out
+    // the VR x TW tile of d out; zero_next (optional): the same block of the other count
+    // buffer cleared for the next iteration's splat (the horizontal pass read it one
+    // iteration ago; clearing it here keeps those stores off the horizontal pass, whose
+    // traffic is a third clears otherwise, and on warps that would idle at the barrier)
     if ((TW & 3) == 0) {
         const int TW4 = TW >> 2, l4 = 31 - __clz(TW4);  // TW is a power of two
         for (int q = threadIdx.x; q < VR * TW4; q += blockDim.x) {
             const int r = q >> l4, c4 = q & (TW4 - 1);
             reinterpret_cast<float4*>(d + (int64_t)(a0 + r) * s + i0)[c4] = reinterpret_cast<const float4*>(sd)[q];
+            if (zero_next)
+                reinterpret_cast<uint4*>(zero_next + (int64_t)(a0 + r) * s + i0)[c4] = make_uint4(0u, 0u, 0u, 0u);
         }
     } else {
         for (int q = threadIdx.x; q < VR * TW; q += blockDim.x) {
             const int r = q / TW, c = q - r * TW;
             d[(int64_t)(a0 + r) * s + i0 + c] = sd[q];
+            if (zero_next) zero_next[(int64_t)(a0 + r) * s + i0 + c] = 0u;
         }
     }
     __syncthreads();

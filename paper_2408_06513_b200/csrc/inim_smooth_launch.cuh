@@ -30,14 +30,15 @@ __global__ void __launch_bounds__(256, CNT ? 4 : 1) smooth_h_kernel(const T* __r
 template <int R>
 __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__ tmp, float* __restrict__ d,
                                                        const Geo g, const VGeo v, const Ws ws, const Taps taps,
-                                                       float background, int emit, const int* state, int64_t zslab) {
+                                                       float background, int emit, const int* state, int64_t zslab,
+                                                       uint32_t* zero_next) {
     pdl_enter();
     state = zstate(state, zslab);
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
     const int64_t zo = zslab_off(zslab);
     smooth_v_tile<R>(zoff(tmp, zo), zoff(d, zo), g, v, ws_shift(ws, zo), taps, background, emit, blockIdx.x,
-                     blockIdx.y, vsm);
+                     blockIdx.y, vsm, zoff_opt(zero_next, zo));
 }
 
 template <int R, typename T, bool CNT>
@@ -57,14 +58,14 @@ inline int launch_h(const T* in, float* out, int s, const Taps& taps, const int*
 
 template <int R>
 inline int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, const Taps& taps, float bg, int emit,
-                    const int* state, cudaStream_t st, const Bat& bt) {
+                    const int* state, cudaStream_t st, const Bat& bt, uint32_t* zero_next = nullptr) {
 
     const VGeo v = make_vgeo(g);
     const size_t smem = v_smem_bytes(g, v, R);
     INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_v_kernel<R>, 227 * 1024));
     dim3 grid(g.NX, g.s / v.VR, bt.B);
     INIM_CUDA_TRY(launch_pdl(smooth_v_kernel<R>, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
-                             state, bt.slab));
+                             state, bt.slab, zero_next));
     prof_mark(st, emit ? "smooth_v_reduce" : "smooth_v");
     return (int)cudaGetLastError();
 }
@@ -74,14 +75,22 @@ template <int KS>
 int launch_pair(const void* in, int kind, const Geo& g, const Ws& ws, const Taps& taps, float bg,
                        float* d, int emit, const int* state, uint32_t* zero_next, cudaStream_t st, const Bat& bt) {
     constexpr int R = 3 * KS;
+    // the clear of the next count buffer rides on the vertical pass (INIM_CLEAR_IN_V=0:
+    // on the horizontal pass, as before)
+    static const bool clear_in_v = [] {
+        const char* e = getenv("INIM_CLEAR_IN_V");
+        return !(e && e[0] == '0');
+    }();
+    uint32_t* zh = clear_in_v ? nullptr : zero_next;
+    uint32_t* zv = clear_in_v ? zero_next : nullptr;
     int rc = kind == 1   ? launch_h<R, uint32_t, true>(static_cast<const uint32_t*>(in), ws.tmp, g.s, taps, state,
-                                                      zero_next, st, bt)
-             : kind == 2 ? launch_h<R, float, true>(static_cast<const float*>(in), ws.tmp, g.s, taps, state,
-                                                   zero_next, st, bt)
-                         : launch_h<R, float, false>(static_cast<const float*>(in), ws.tmp, g.s, taps, state,
-                                                    zero_next, st, bt);
+                                                      zh, st, bt)
+             : kind == 2 ? launch_h<R, float, true>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zh, st,
+                                                   bt)
+                         : launch_h<R, float, false>(static_cast<const float*>(in), ws.tmp, g.s, taps, state, zh,
+                                                    st, bt);
     if (rc) return rc;
-    return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st, bt);
+    return launch_v<R>(ws.tmp, d, g, ws, taps, bg, emit, state, st, bt, zv);
 }
 
 }  // namespace inim
