@@ -218,6 +218,17 @@ __host__ __device__ __forceinline__ Ws ws_shift(Ws w, int64_t b) {
 // byte offset of this CTA's plot
 INIM_DEV int64_t zslab_off(int64_t slab) { return (int64_t)blockIdx.z * slab; }
 
+// INIM_ZREV=0: every batched kernel walks the plots in launch order.  Otherwise the
+// vertical pass and the move walk them backwards, so each consumer starts on the plots
+// its producer wrote last (still in L2): h up, v down, write up, move down.
+inline bool zrev_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("INIM_ZREV");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // the run's device state word pair {stopped, iterations done} of this CTA's plot: one
 // per plot, inside its workspace slab, in a batch
 INIM_DEV const int* zstate(const int* state, int64_t slab) { return state ? zoff(state, zslab_off(slab)) : state; }

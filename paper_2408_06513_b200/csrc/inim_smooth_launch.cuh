@@ -31,12 +31,12 @@ template <int R>
 __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__ tmp, float* __restrict__ d,
                                                        const Geo g, const VGeo v, const Ws ws, const Taps taps,
                                                        float background, int emit, const int* state, int64_t zslab,
-                                                       uint32_t* zero_next) {
+                                                       uint32_t* zero_next, int zrev) {
     pdl_enter();
-    state = zstate(state, zslab);
+    const int64_t zo = (zrev ? (int64_t)(gridDim.z - 1 - blockIdx.z) : (int64_t)blockIdx.z) * zslab;
+    state = zoff_opt(state, zo);
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
-    const int64_t zo = zslab_off(zslab);
     smooth_v_tile<R>(zoff(tmp, zo), zoff(d, zo), g, v, ws_shift(ws, zo), taps, background, emit, blockIdx.x,
                      blockIdx.y, vsm, zoff_opt(zero_next, zo));
 }
@@ -65,7 +65,7 @@ inline int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, cons
     INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_v_kernel<R>, 227 * 1024));
     dim3 grid(g.NX, g.s / v.VR, bt.B);
     INIM_CUDA_TRY(launch_pdl(smooth_v_kernel<R>, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
-                             state, bt.slab, zero_next));
+                             state, bt.slab, zero_next, bt.B > 1 && zrev_enabled() ? 1 : 0));
     prof_mark(st, emit ? "smooth_v_reduce" : "smooth_v");
     return (int)cudaGetLastError();
 }

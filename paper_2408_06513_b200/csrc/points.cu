@@ -290,13 +290,17 @@ __global__ void __launch_bounds__(256) move_bulk_kernel(const float* __restrict_
                                                         const float* __restrict__ in, float* __restrict__ out,
                                                         int64_t n, int clip, float* max_disp, const int* state,
                                                         uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
-                                                        int agg, int64_t zin, int64_t zout, int64_t zslab) {
+                                                        int agg, int64_t zin, int64_t zout, int64_t zslab,
+                                                        int zrev) {
     __shared__ __align__(128) float4 buf[2][kMoveChunk];
     __shared__ __align__(8) uint64_t bar[2];
-    const int64_t zo = zslab_off(zslab);
+    // zrev: plots in reverse launch order, so the move starts on the plots whose fields
+    // the write pass produced last (still in L2)
+    const int64_t zi = zrev ? (int64_t)(gridDim.z - 1 - blockIdx.z) : (int64_t)blockIdx.z;
+    const int64_t zo = zi * zslab;
     tg = zoff(tg, zo);
-    in += blockIdx.z * zin;
-    out += blockIdx.z * zout;
+    in += zi * zin;
+    out += zi * zout;
     max_disp = zoff_opt(max_disp, zo);
     splat_next = zoff_opt(splat_next, zo);
     zn0 = zoff_opt(zn0, zo);
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(256) move_bulk_kernel(const float* __restrict_
     }
     __syncthreads();
     pdl_enter();
-    state = zstate(state, zslab);
+    state = zoff_opt(state, zo);
     const bool stopped = state && state[0];
     const int s = 1 << k;
     if (splat_next && !stopped && blockIdx.x == 0 && tid == 0) {
@@ -691,7 +695,7 @@ int launch_sample_f32(const float* tg, int k, const float* in, float* out, int64
         const int64_t per_plot = (nchunk + bulk_cpc - 1) / bulk_cpc;
         INIM_CUDA_TRY(launch_pdl(kb, dim3((unsigned)per_plot, 1, (unsigned)bt.B), dim3(256), 0, st, tg, k, in, out, n,
                                  clip, max_disp, state, splat_next, zn0, zn1, sorted ? (f32_counts ? 2 : 1) : 0, zin,
-                                 zout, bt.slab));
+                                 zout, bt.slab, zrev_enabled() ? 1 : 0));
         prof_mark(st, "sample");
         return (int)cudaGetLastError();
     }
