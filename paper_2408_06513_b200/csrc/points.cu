@@ -285,8 +285,10 @@ __global__ void __launch_bounds__(256) sample_f32_kernel(const float* __restrict
 constexpr int kMoveU = INIM_BULK_U;
 constexpr int kMoveChunk = 256 * kMoveU;  // pairs per chunk (8 KB)
 
+// Six CTAs per SM (40 registers): 48 warps of gathers in flight per SM (C4 -0.9% against
+// five at 48 registers; seven spill).
 template <bool PAIRS>
-__global__ void __launch_bounds__(256) move_bulk_kernel(const float* __restrict__ tg, int k,
+__global__ void __launch_bounds__(256, 6) move_bulk_kernel(const float* __restrict__ tg, int k,
                                                         const float* __restrict__ in, float* __restrict__ out,
                                                         int64_t n, int clip, float* max_disp, const int* state,
                                                         uint32_t* __restrict__ splat_next, float* zn0, float* zn1,
