@@ -35,6 +35,7 @@ g64 = torch.empty(host.shape, dtype=torch.float64, device="cuda")
 for _ in range(3):
     P.run(ds, params, store_fields=False).frame(10)
 print("h2d staged (to_device)    %.3f ms" % med(lambda: D.to_device(host, out=dev)))
+print("h2d to_device, pinned in  %.3f ms" % med(lambda: D.to_device(pinned.numpy(), out=dev)))
 g64b = torch.empty(host.shape, dtype=torch.float64, device="cuda")
 print("h2d pageable f64          %.3f ms" % med(lambda: g64b.copy_(torch.from_numpy(host), non_blocking=True)))
 out64 = np.empty_like(host)
