@@ -9,6 +9,8 @@
                     eight chunks per CTA) at plot sizes that leave partial chunks, a
                     single chunk, a single pair, and CTAs with fewer than eight chunks:
                     against each plot regularized alone and against the oracle
+  runtime switches  every INIM_* switch of INTEGRATION.md section 5 leaves single-plot and
+                    batched results bit-identical
 """
 
 import numpy as np
@@ -50,3 +52,46 @@ def test_batch_move_partial_chunks(P, oracle, points):
                   store_fields=False)
         assert maxerr(res[i], r.frame(iters)) <= POS_TOL, (points, i)
         assert maxerr(res[i], oracle.run_positions(pts, 8, 8, iters)[-1]) <= POS_TOL, (points, i)
+
+
+SWITCH_SCRIPT = """
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import paper_2408_06513_b200 as P
+from paper_2408_06513_b200.splom import DeviceSplom, SplomConfig, splom_plot
+host = np.load({inp!r})
+r = P.run(P.ScatterDataset(positions=host), P.RegularizationParams(k=10, kernel_size=8, iterations=4),
+          store_fields=False)
+cfg = SplomConfig(nplots=6, points=70_000, k=9, kernel_size=8, iterations=4, collect_metrics=True)
+job = DeviceSplom(cfg, range(cfg.nplots))
+job.load(lambda i: splom_plot(i, cfg.points))
+pos = job.run().cpu().numpy()
+np.savez({out!r}, single=r.frame(4), batch=pos, met=np.asarray(job.metrics(), dtype=np.float64))
+"""
+
+
+@pytest.mark.parametrize("switch", ["INIM_V_EMIT=0", "INIM_MOVE_BULK=0", "INIM_CLEAR_IN_V=0", "INIM_ZREV=0",
+                                    "INIM_SORT=0", "INIM_PDL=0"])
+def test_runtime_switches_bit_identical(tmp_path, switch):
+    """none of the runtime switches changes a result.  One
+    single-plot run (sorted path) and one batched SPLOM run with frame statistics, with
+    the switch and without, compared bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    np.save(tmp_path / "in.npy", clusters(200_000, 10).astype(np.float64))
+    outs = []
+    for tag, env in (("base", {}), ("sw", dict([switch.split("=")]))):
+        dst = tmp_path / f"{tag}.npz"
+        f = tmp_path / f"{tag}.py"
+        f.write_text(SWITCH_SCRIPT.format(root=str(ROOT), inp=str(tmp_path / "in.npy"), out=str(dst)))
+        run = subprocess.run([sys.executable, str(f)], capture_output=True, text=True, timeout=300,
+                             env=dict(os.environ, **env))
+        assert run.returncode == 0, run.stderr[-2000:]
+        outs.append(np.load(dst))
+    for key in ("single", "batch", "met"):
+        assert np.array_equal(outs[0][key], outs[1][key]), (switch, key)
