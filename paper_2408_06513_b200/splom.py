@@ -32,14 +32,22 @@ def shard(nplots: int, world: int, rank: int) -> range:
 
 
 def _chunk_bounds(nb: int, chunk: int, lead: int) -> list:
-    """[b0, b1) plot ranges for run_host: `lead` plots first and last, the rest in
-    near-equal chunks of at most `chunk`."""
-    if lead <= 0 or nb <= 2 * lead + chunk:
+    """[b0, b1) plot ranges for run_host.  The copy in of the first chunk and the copy out
+    of the last are the parts nothing overlaps, so the chunks ramp: `lead` plots, then
+    doubling up to `chunk`, the middle in near-equal chunks of at most `chunk`, and the
+    mirror image at the end (a batched run computes a plot in about twice the time its
+    copy takes, so each chunk's copy hides behind the previous chunk's run)."""
+    if lead <= 0 or lead >= chunk or nb < 3 * lead:
         sizes = [chunk] * (nb // chunk) + ([nb % chunk] if nb % chunk else [])
     else:
-        mid = nb - 2 * lead
+        ramp = []
+        c = lead
+        while c < chunk and 2 * (sum(ramp) + c) + c <= nb:  # leaves a middle at least c
+            ramp.append(c)
+            c *= 2
+        mid = nb - 2 * sum(ramp)
         k = -(-mid // chunk)
-        sizes = [lead] + [mid // k + (1 if q < mid % k else 0) for q in range(k)] + [lead]
+        sizes = ramp + [mid // k + (1 if q < mid % k else 0) for q in range(k)] + ramp[::-1]
     out, b0 = [], 0
     for n in sizes:
         out.append((b0, b0 + n))
@@ -140,13 +148,14 @@ class DeviceSplom:
                 on_chunk(b0, b1)
         return self.work
 
-    def run_host(self, host_in, host_out, chunk: int = 64, lead: int = 32):
+    def run_host(self, host_in, host_out, chunk: int = 96, lead: int = 8):
         """The whole block from page-locked host buffers: (B, n, 2) float32 in, final
         positions out.  The plots go in chunks of about `chunk`: chunk c + 1 is copied in
         on one copy stream and chunk c - 1 copied out on another while chunk c runs (the
         copy engines work beside the SMs), so the step costs about max(compute,
-        transfers) instead of their sum.  The first and the last chunk hold only `lead`
-        plots: their copy in / out is the part nothing overlaps.  Returns host_out."""
+        transfers) instead of their sum.  The chunks ramp from `lead` plots up and back
+        down (_chunk_bounds): the first copy in and the last copy out are the parts
+        nothing overlaps.  Returns host_out."""
         torch, D, lib, cfg = self.torch, self.D, self.lib, self.cfg
         nb = len(self.ids)
         chunk = max(1, min(chunk, self.batch))

@@ -19,7 +19,7 @@ job.load(lambda i: cache.setdefault(i % 16, splom_plot(i % 16, cfg.points)))
 host_in = torch.empty(tuple(job.inputs.shape), dtype=torch.float32).pin_memory()
 host_in.copy_(job.inputs.cpu())
 host_out = torch.empty_like(host_in).pin_memory()
-for chunk, lead in [(64, 32), (96, 32), (64, 48), (48, 24), (128, 32), (80, 40)]:
+for chunk, lead in [(96, 8), (96, 0), (64, 32), (96, 4)]:
     def call():
         job.run_host(host_in, host_out, chunk=chunk, lead=lead)
         torch.cuda.current_stream().synchronize()
