@@ -420,9 +420,12 @@ __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const 
 #pragma unroll
         for (int e = 0; e < CPL; ++e) dnext[e] = __ldg(defrow + e);
     }
-    // GSRC: a ring of PF rows in flight per lane, refilled as rows retire; with two
-    // columns per lane (16-row tiles) the whole tile is requested up front
-    constexpr int PF = GSRC ? (CPL <= 2 ? 16 : 2) : 1;
+    // GSRC: a ring of PF rows in flight per lane, refilled as rows retire; the tables
+    // pass with two columns per lane (16-row tiles) requests the whole tile up front.  The
+    // field pass keeps a two-row ring there too: its fully unrolled 16-row sweep was 4k
+    // instructions of code per warp, fetched anew in every iteration of a graph replay
+    // (C2 44.4 -> 43.4 us per iteration with the ring)
+    constexpr int PF = GSRC ? (CPL <= 2 && MODE == 0 ? 16 : 2) : 1;
     float ring[PF][CPL];
     if (GSRC) {
 #pragma unroll
