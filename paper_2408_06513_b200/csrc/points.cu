@@ -455,13 +455,26 @@ __global__ void __launch_bounds__(1024) scan_top_kernel(uint32_t* __restrict__ b
     }
 }
 
+// self_prefix: bsum holds the raw block sums and each block adds up its predecessors'
+// itself (up to kScanSelfMax blocks: a strided block reduction, exact integers), so the
+// one-CTA scan_top launch is skipped; otherwise bsum is already scanned by scan_top.
+constexpr int kScanSelfMax = 8192;
+
 __global__ void __launch_bounds__(256) scan_blocks_kernel(const uint32_t* __restrict__ counts, int64_t m,
                                                           const uint32_t* __restrict__ bsum,
-                                                          uint32_t* __restrict__ offsets, int64_t zslab) {
+                                                          uint32_t* __restrict__ offsets, int64_t zslab,
+                                                          int self_prefix) {
     pdl_enter();
     counts = zoff(counts, zslab_off(zslab));
     bsum = zoff(bsum, zslab_off(zslab));
     offsets = zoff(offsets, zslab_off(zslab));
+    __shared__ uint32_t pre[8];
+    if (self_prefix) {
+        uint32_t a = 0;
+        for (int q = threadIdx.x; q < (int)blockIdx.x; q += blockDim.x) a += __ldcg(bsum + q);
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(kFull, a, o);
+        if ((threadIdx.x & 31) == 0) pre[threadIdx.x >> 5] = a;
+    }
     const int64_t base = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
     uint32_t c[kScanItems];
     uint32_t v = 0;
@@ -481,7 +494,14 @@ __global__ void __launch_bounds__(256) scan_blocks_kernel(const uint32_t* __rest
     __shared__ uint32_t ws[8];
     if (lane == 31) ws[w] = inc;
     __syncthreads();
-    uint32_t run = bsum[blockIdx.x] + inc - v;
+    uint32_t blk = 0;
+    if (self_prefix) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) blk += pre[q];
+    } else {
+        blk = bsum[blockIdx.x];
+    }
+    uint32_t run = blk + inc - v;
     for (int q = 0; q < w; ++q) run += ws[q];
 #pragma unroll
     for (int q = 0; q < kScanItems; q += 4) {
@@ -633,9 +653,11 @@ int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* count
     const unsigned nb = (unsigned)((m + kScanBlock - 1) / kScanBlock);
     const unsigned z = (unsigned)bt.B;
     INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb, 1, z), dim3(256), 0, st, counts, m, bsum, bt.slab));
-    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1, 1, z), dim3(1024), 0, st, bsum, (int)nb, bt.slab));
+    const int self_prefix = nb <= (unsigned)kScanSelfMax ? 1 : 0;
+    if (!self_prefix)
+        INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1, 1, z), dim3(1024), 0, st, bsum, (int)nb, bt.slab));
     INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb, 1, z), dim3(256), 0, st, counts, m, (const uint32_t*)bsum,
-                             cursor, bt.slab));
+                             cursor, bt.slab, self_prefix));
     INIM_CUDA_TRY(launch_pdl(place_points_kernel, batch_grid(grid_for(n > 0 ? n : 1, 256), n, 256, bt), dim3(256), 0,
                              st, reinterpret_cast<const float2*>(pts), n, k, cursor, reinterpret_cast<float2*>(sorted),
                              rank, bt.pts, bt.slab));
@@ -647,9 +669,11 @@ int launch_sort_points(const float* pts, int64_t n, int k, const uint32_t* count
 int launch_exclusive_scan_u32(const uint32_t* counts, int64_t m, uint32_t* bsum, uint32_t* out, cudaStream_t st) {
     const unsigned nb = (unsigned)((m + kScanBlock - 1) / kScanBlock);
     INIM_CUDA_TRY(launch_pdl(scan_block_sums_kernel, dim3(nb), dim3(256), 0, st, counts, m, bsum, (int64_t)0));
-    INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb, (int64_t)0));
+    const int self_prefix = nb <= (unsigned)kScanSelfMax ? 1 : 0;
+    if (!self_prefix)
+        INIM_CUDA_TRY(launch_pdl(scan_top_kernel, dim3(1), dim3(1024), 0, st, bsum, (int)nb, (int64_t)0));
     INIM_CUDA_TRY(launch_pdl(scan_blocks_kernel, dim3(nb), dim3(256), 0, st, counts, m, (const uint32_t*)bsum, out,
-                             (int64_t)0));
+                             (int64_t)0, self_prefix));
     return (int)cudaGetLastError();
 }
 
