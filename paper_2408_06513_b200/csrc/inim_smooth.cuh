@@ -399,12 +399,21 @@ __host__ __device__ inline size_t v_smem_bytes(const Geo& g, const VGeo& v, int 
 
 // Vertical pass + background of tile (bx, by) = VB bands x TW columns; with `emit`,
 // each band's tile of d goes straight from shared memory into the tile reduce.
-template <int R>
+// VG: the two geometries the runs use as compile-time constants (1: 32 x 128 bands of
+// batches and grids above 2048^2, 2: the 16 x 64 bands up to 2048^2, both 64-row CTAs of
+// 256 threads), so the staging, FIR and reduce dispatch and the store loop fold; 0: the
+// runtime geometry of small grids.
+template <int R, int VG = 0>
 __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, float* __restrict__ d, const Geo& g,
                                               const VGeo& v, const Ws& ws, const Taps& taps, float background,
                                               int emit, int bx, int by, float* vsm, uint32_t* zero_next = nullptr) {
-    const int TH = g.TH, TW = g.TW, s = g.s, VR = v.VR;
-    const bool inplace = v_inplace(TH, TW, v.GT);
+    const int TH = VG == 1 ? 32 : (VG == 2 ? 16 : g.TH);
+    const int TW = VG == 1 ? 128 : (VG == 2 ? 64 : g.TW);
+    const int VR = VG ? 64 : v.VR, VB = VG == 1 ? 2 : (VG == 2 ? 4 : v.VB), GT = VG ? TW : v.GT;
+    const int CPL = VG == 1 ? 4 : (VG == 2 ? 2 : g.CPL);
+    const int NT = VG ? 256 : (int)blockDim.x;
+    const int s = g.s;
+    const bool inplace = VG ? true : v_inplace(TH, TW, GT);
     float* sh = vsm;                                                 // [(VR + 2R)][TW]
     float* sd = inplace ? vsm : vsm + (size_t)(VR + 2 * R) * TW;     // [VR][TW]  d for VB bands
     const int x = bx;
@@ -416,8 +425,8 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
         // once as an asynchronous global -> shared copy (cp.async.cg, no register
         // staging), so the tile costs one memory round trip
         const int TW4 = TW >> 2;
-        const int cpr = TW4 < (int)blockDim.x ? TW4 : (int)blockDim.x;  // threads per row
-        const int rpp = blockDim.x / cpr;                                // rows per pass
+        const int cpr = TW4 < NT ? TW4 : NT;  // threads per row
+        const int rpp = NT / cpr;              // rows per pass
         const int c4 = threadIdx.x % cpr;
         if (c4 < TW4) {
             for (int r = threadIdx.x / cpr; r < H; r += rpp) {
@@ -457,12 +466,12 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
         }
     }
     __syncthreads();
-    const int grp = threadIdx.x / v.GT, tid = threadIdx.x - grp * v.GT;
+    const int grp = threadIdx.x / GT, tid = threadIdx.x - grp * GT;
     if (inplace) {  // (the branch is uniform over the CTA: it contains a barrier)
-        const bool live = grp < v.VB;
+        const bool live = grp < VB;
         if (TH == 32) fir_cols4_inplace<R, 8>(sh, TW, grp * TH, tid, live, background);
         else fir_cols4_inplace<R, 4>(sh, TW, grp * TH, tid, live, background);
-    } else if (grp < v.VB && tid < TW) {
+    } else if (grp < VB && tid < TW) {
         const int rb = grp * TH;  // first row of this group's band within the CTA
         fir_line<R, 8>(
             taps, TH, [&](int q) { return sh[(rb + q) * TW + tid]; },
@@ -471,12 +480,12 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     __syncthreads();
     if (emit) {
         // one warp per band tile of d, straight from shared memory
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-        for (int gb = warp; gb < v.VB; gb += nwarps) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = NT >> 5;
+        for (int gb = warp; gb < VB; gb += nwarps) {
             const float* src = sd + (size_t)gb * TH * TW;
             const int b = a0 / TH + gb;
-            if (g.CPL == 4) warp_tile_reduce<4>(src, TW, g, ws, b, x, lane);
-            else if (g.CPL == 2) warp_tile_reduce<2>(src, TW, g, ws, b, x, lane);
+            if (CPL == 4) warp_tile_reduce<4>(src, TW, g, ws, b, x, lane);
+            else if (CPL == 2) warp_tile_reduce<2>(src, TW, g, ws, b, x, lane);
             else warp_tile_reduce<1>(src, TW, g, ws, b, x, lane);
         }
     }
@@ -485,8 +494,8 @@ __device__ __forceinline__ void smooth_v_tile(const float* __restrict__ tmp, flo
     // iteration ago; clearing it here keeps those stores off the horizontal pass, whose
     // traffic is a third clears otherwise, and on warps that would idle at the barrier)
     if ((TW & 3) == 0) {
-        const int TW4 = TW >> 2, l4 = 31 - __clz(TW4);  // TW is a power of two
-        for (int q = threadIdx.x; q < VR * TW4; q += blockDim.x) {
+        const int TW4 = TW >> 2, l4 = VG == 1 ? 5 : (VG == 2 ? 4 : 31 - __clz(TW4));  // TW is a power of two
+        for (int q = threadIdx.x; q < VR * TW4; q += NT) {
             const int r = q >> l4, c4 = q & (TW4 - 1);
             reinterpret_cast<float4*>(d + (int64_t)(a0 + r) * s + i0)[c4] = reinterpret_cast<const float4*>(sd)[q];
             if (zero_next)

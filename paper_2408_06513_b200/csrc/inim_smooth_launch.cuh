@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256, CNT ? 4 : 1) smooth_h_kernel(const T* __r
     smooth_h_tile<R, T, CNT, FULL>(in, out, s, h, taps, zero_next, blockIdx.x, blockIdx.y, hsm);
 }
 
-template <int R>
+template <int R, int VG>
 __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__ tmp, float* __restrict__ d,
                                                        const Geo g, const VGeo v, const Ws ws, const Taps taps,
                                                        float background, int emit, const int* state, int64_t zslab,
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(512) smooth_v_kernel(const float* __restrict__
     state = zoff_opt(state, zo);
     if (state && state[0]) return;
     extern __shared__ __align__(16) float vsm[];
-    smooth_v_tile<R>(zoff(tmp, zo), zoff(d, zo), g, v, ws_shift(ws, zo), taps, background, emit, blockIdx.x,
+    smooth_v_tile<R, VG>(zoff(tmp, zo), zoff(d, zo), g, v, ws_shift(ws, zo), taps, background, emit, blockIdx.x,
                      blockIdx.y, vsm, zoff_opt(zero_next, zo));
 }
 
@@ -62,9 +62,13 @@ inline int launch_v(const float* tmp, float* d, const Geo& g, const Ws& ws, cons
 
     const VGeo v = make_vgeo(g);
     const size_t smem = v_smem_bytes(g, v, R);
-    INIM_CUDA_TRY(ensure_smem_limit((const void*)smooth_v_kernel<R>, 227 * 1024));
+    // the two geometries of the runs as compile-time constants (smooth_v_tile VG)
+    const bool vg1 = g.TH == 32 && g.TW == 128 && g.CPL == 4 && v.VR == 64 && v.VB == 2 && v.GT == 128;
+    const bool vg2 = g.TH == 16 && g.TW == 64 && g.CPL == 2 && v.VR == 64 && v.VB == 4 && v.GT == 64;
+    auto kern = vg1 ? smooth_v_kernel<R, 1> : (vg2 ? smooth_v_kernel<R, 2> : smooth_v_kernel<R, 0>);
+    INIM_CUDA_TRY(ensure_smem_limit((const void*)kern, 227 * 1024));
     dim3 grid(g.NX, g.s / v.VR, bt.B);
-    INIM_CUDA_TRY(launch_pdl(smooth_v_kernel<R>, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
+    INIM_CUDA_TRY(launch_pdl(kern, grid, dim3(v.VB * v.GT), smem, st, tmp, d, g, v, ws, taps, bg, emit,
                              state, bt.slab, zero_next, bt.B > 1 && zrev_enabled() ? 1 : 0));
     prof_mark(st, emit ? "smooth_v_reduce" : "smooth_v");
     return (int)cudaGetLastError();
