@@ -297,11 +297,14 @@ INIM_DEV int64_t flat_dsuf_count(int dl, int s) {  // #{i' - j' >= dl}
 // explicit defect array (build_field with a caller-supplied flat response).
 // GSRC: `src` is the tile origin in global memory (row stride ld) and rows are fetched
 // two ahead into registers; otherwise `src` is a staged (shared-memory) tile.
-template <int CPL, int MODE, bool GSRC = false>
+// GEO: the run geometry as compile-time constants (TW = 32 CPL with every lane holding
+// columns, TH = 32 for CPL = 4, 16 for CPL = 2), so the row sweep and the per-row lane
+// tests fold; the caller checks the geometry (and uses it for the 16 x 64 tiles only).
+template <int CPL, int MODE, bool GSRC = false, bool GEO = false>
 __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
                                                 int lane, const WriteOut out) {
-    const int TH = g.TH, TW = g.TW, s = g.s, NX = g.NX, B = g.B;
-    const int last = g.WL - 1;
+    const int TH = GEO ? (CPL == 4 ? 32 : 16) : g.TH, TW = GEO ? 32 * CPL : g.TW, s = g.s, NX = g.NX, B = g.B;
+    const int last = GEO ? 31 : g.WL - 1;
     const int u0 = lane * CPL;
     const bool act = lane <= last;
     const int a = b * TH, i0 = x * TW;

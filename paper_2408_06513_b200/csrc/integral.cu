@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) reduce_kernel(const float* 
 
 // The write pass re-reads its tile straight from global memory (rows prefetched two
 // ahead in registers): no shared memory, so residency is bounded by registers only.
-template <int CPL, int MODE>
+template <int CPL, int MODE, bool GEO = false>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, CPL == 4 ? 5 : 1) write_kernel(const float* __restrict__ d, const Geo g,
                                                                   const Ws ws0, const WriteOut out0, const int* state,
                                                                   int64_t zslab) {
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, CPL == 4 ? 5 : 1) write_ker
     if (tile >= g.B * g.NX) return;
     const int b = tile / g.NX, x = tile - b * g.NX;
     const float* src = d + (int64_t)b * g.TH * g.s + (int64_t)x * g.TW;
-    warp_tile_write<CPL, MODE, true>(src, g.s, g, ws, b, x, lane, out);
+    warp_tile_write<CPL, MODE, true, GEO>(src, g.s, g, ws, b, x, lane, out);
 }
 
 // ---- standalone helpers --------------------------------------------------------------
@@ -276,8 +276,14 @@ int launch_reduce_from_global(const float* d, const Geo& g, const Ws& ws, const 
 template <int CPL, int MODE>
 static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const WriteOut& out, const int* state,
                             cudaStream_t st, const Bat& bt) {
-    INIM_CUDA_TRY(launch_pdl(write_kernel<CPL, MODE>, dim3(tile_ctas(g), 1, bt.B), dim3(kWarpsPerCta * 32), 0, st, d,
-                             g, ws, out, state, bt.slab));
+    // the 16 x 64 tiles of grids up to 2048^2 as compile-time constants (C2 41.4 -> 40.45
+    // us per iteration; the 32 x 128 instance spills at its 96-register cap and is slower)
+    auto kern = write_kernel<CPL, MODE>;
+    if constexpr (MODE != 0 && CPL == 2) {
+        if (g.WL == 32 && g.TW == 64 && g.TH == 16) kern = write_kernel<CPL, MODE, true>;
+    }
+    INIM_CUDA_TRY(launch_pdl(kern, dim3(tile_ctas(g), 1, bt.B), dim3(kWarpsPerCta * 32), 0, st, d, g, ws, out, state,
+                             bt.slab));
     prof_mark(st, MODE == 0 ? "write_tables" : "write_field");
     return (int)cudaGetLastError();
 }
