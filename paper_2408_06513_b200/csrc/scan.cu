@@ -7,16 +7,34 @@
 
 namespace inim {
 
+// The run tile geometries as compile-time constants of a local Geo (GEO 1: 32 x 128
+// tiles, 2: 16 x 64 tiles, 0: as passed), so the index arithmetic of the scans folds.
+template <int GEO>
+__device__ __forceinline__ Geo fixed_geo(const Geo& g) {
+    Geo f = g;
+    if (GEO == 1) { f.TH = 32; f.TW = 128; f.twlog = 7; f.CPL = 4; f.WL = 32; }
+    if (GEO == 2) { f.TH = 16; f.TW = 64; f.twlog = 6; f.CPL = 2; f.WL = 32; }
+    return f;
+}
+
+inline int geo_kind(const Geo& g) {
+    if (g.WL != 32) return 0;
+    if (g.TH == 32 && g.TW == 128) return 1;
+    if (g.TH == 16 && g.TW == 64) return 2;
+    return 0;
+}
+
 // Launch bounds: the plain 512-thread bound settles at 40 registers (3 CTAs/SM),
 // measured best (an explicit minimum of 1 CTA/SM lets ptxas spend 72
 // registers and costs 4% of the 16384^2 integral pass; 4 CTAs/SM spill).  BATCH: the
 // plot offsets of a SPLOM batch (grid.z) are a separate instantiation, so the
 // single-plot kernels keep their register budget.
-template <bool BATCH>
-__global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
+template <bool BATCH, int GEO = 0>
+__global__ void __launch_bounds__(512) chains_kernel(const Geo g0, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
     if (BATCH) state = zstate(state, zslab);
     if (state && state[0]) return;
+    const Geo g = fixed_geo<GEO>(g0);
     const Ws ws = BATCH ? ws_shift(ws0, zslab_off(zslab)) : ws0;
     __shared__ double part[16][33];
     __shared__ double bp[kMaxBands + 1];
@@ -33,11 +51,12 @@ __global__ void __launch_bounds__(512) chains_kernel(const Geo g, const Ws ws0, 
 }
 
 // Single-read chains: each thread holds its chunk of step terms in registers.
-template <int MAXCH, bool BATCH>
-__global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
+template <int MAXCH, bool BATCH, int GEO = 0>
+__global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g0, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
     if (BATCH) state = zstate(state, zslab);
     if (state && state[0]) return;
+    const Geo g = fixed_geo<GEO>(g0);
     const Ws ws = BATCH ? ws_shift(ws0, zslab_off(zslab)) : ws0;
     __shared__ double part[16][33];
     __shared__ double bp[kMaxBands + 1];
@@ -49,8 +68,10 @@ __global__ void __launch_bounds__(512) chains_reg_kernel(const Geo g, const Ws w
 // tiles of row j's tile row sums, rpre = the band's in-band prefix of the row totals,
 // tilepre / btot = the exclusive prefix and the total of the band's tile totals.  A
 // launch of its own so that no reduce warp has to fence and count its band's arrivals.
-__global__ void __launch_bounds__(1024) lines_kernel(const Geo g, const Ws ws0, const int* state, int64_t zslab) {
+template <int GEO>
+__global__ void __launch_bounds__(1024) lines_kernel(const Geo g0, const Ws ws0, const int* state, int64_t zslab) {
     pdl_enter();
+    const Geo g = fixed_geo<GEO>(g0);
     state = zstate(state, zslab);
     if (state && state[0]) return;
     const Ws ws = ws_shift(ws0, zslab_off(zslab));
@@ -92,7 +113,9 @@ int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaSt
     // band-total scan runs on warp 1)
     int lt = g.NX < 32 ? (g.TH * g.NX + 31) / 32 * 32 : 32 * g.TH;
     if (lt < 64) lt = 64;
-    INIM_CUDA_TRY(launch_pdl(lines_kernel, dim3(g.B, 1, bt.B), dim3(lt), 0, st, g, ws, state, bt.slab));
+    const int gk = geo_kind(g);
+    auto lk = gk == 1 ? lines_kernel<1> : (gk == 2 ? lines_kernel<2> : lines_kernel<0>);
+    INIM_CUDA_TRY(launch_pdl(lk, dim3(g.B, 1, bt.B), dim3(lt), 0, st, g, ws, state, bt.slab));
     prof_mark(st, "lines");
     const bool batch = bt.B > 1;
     static const int batch_per = [] {  // INIM_CHAIN_PER: step terms per thread in a batch (4 or 8)
@@ -105,8 +128,9 @@ int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaSt
     const int ny = chain_warps(g, per), ch = (g.B + ny - 1) / ny;
     const dim3 grid(chains_items(g), 1, bt.B), block(32 * ny);
     if (batch && ch > 4 && ch <= 16) {
-        INIM_CUDA_TRY(launch_pdl(ch <= 8 ? chains_reg_kernel<8, true> : chains_reg_kernel<16, true>, grid, block, 0,
-                                 st, g, ws, state, bt.slab));
+        auto kern = ch <= 8 ? (gk == 1 ? chains_reg_kernel<8, true, 1> : chains_reg_kernel<8, true>)
+                            : chains_reg_kernel<16, true>;
+        INIM_CUDA_TRY(launch_pdl(kern, grid, block, 0, st, g, ws, state, bt.slab));
         prof_mark(st, "chains");
         return (int)cudaGetLastError();
     }
@@ -114,11 +138,13 @@ int launch_carry_scan_state(const Geo& g, const Ws& ws, const int* state, cudaSt
     // the integral sweep; 4096^2 +-0; 8192^2 and up -10%, occupancy); longer chunks run
     // the two-pass kernel
     if (ch <= 4) {
-        INIM_CUDA_TRY(launch_pdl(batch ? chains_reg_kernel<4, true> : chains_reg_kernel<4, false>, grid, block, 0, st,
-                                 g, ws, state, bt.slab));
+        auto kern = batch ? chains_reg_kernel<4, true>
+                          : (gk == 2 ? chains_reg_kernel<4, false, 2> : chains_reg_kernel<4, false>);
+        INIM_CUDA_TRY(launch_pdl(kern, grid, block, 0, st, g, ws, state, bt.slab));
     } else {
-        INIM_CUDA_TRY(launch_pdl(batch ? chains_kernel<true> : chains_kernel<false>, grid, block, 0, st, g, ws, state,
-                                 bt.slab));
+        // (no compile-time geometry here: it costs this kernel 16 registers and a CTA per SM)
+        auto kern = batch ? chains_kernel<true> : chains_kernel<false>;
+        INIM_CUDA_TRY(launch_pdl(kern, grid, block, 0, st, g, ws, state, bt.slab));
     }
     prof_mark(st, "chains");
     return (int)cudaGetLastError();
