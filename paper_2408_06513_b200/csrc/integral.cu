@@ -278,9 +278,11 @@ static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const Wr
                             cudaStream_t st, const Bat& bt) {
     // the 16 x 64 tiles of grids up to 2048^2 as compile-time constants (C2 41.4 -> 40.45
     // us per iteration; the 32 x 128 instance spills at its 96-register cap and is slower)
+    // (tables pass: below 2048^2 only -- its constant-geometry instance holds the whole
+    // tile in 250 registers: 512^2 +8%, 1024^2 +11%, 2048^2 -9% on the integral sweep)
     auto kern = write_kernel<CPL, MODE>;
-    if constexpr (MODE != 0 && CPL == 2) {
-        if (g.WL == 32 && g.TW == 64 && g.TH == 16) kern = write_kernel<CPL, MODE, true>;
+    if constexpr (CPL == 2) {
+        if (g.WL == 32 && g.TW == 64 && g.TH == 16 && (MODE != 0 || g.s < 2048)) kern = write_kernel<CPL, MODE, true>;
     }
     INIM_CUDA_TRY(launch_pdl(kern, dim3(tile_ctas(g), 1, bt.B), dim3(kWarpsPerCta * 32), 0, st, d, g, ws, out, state,
                              bt.slab));
