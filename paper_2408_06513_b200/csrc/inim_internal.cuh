@@ -218,6 +218,23 @@ __host__ __device__ __forceinline__ Ws ws_shift(Ws w, int64_t b) {
 // byte offset of this CTA's plot
 INIM_DEV int64_t zslab_off(int64_t slab) { return (int64_t)blockIdx.z * slab; }
 
+// The run tile geometries as compile-time constants of a local Geo (GEO 1: 32 x 128
+// tiles, 2: 16 x 64 tiles, 0: as passed), so the index arithmetic of the scans folds.
+template <int GEO>
+__device__ __forceinline__ Geo fixed_geo(const Geo& g) {
+    Geo f = g;
+    if (GEO == 1) { f.TH = 32; f.TW = 128; f.twlog = 7; f.CPL = 4; f.WL = 32; }
+    if (GEO == 2) { f.TH = 16; f.TW = 64; f.twlog = 6; f.CPL = 2; f.WL = 32; }
+    return f;
+}
+
+inline int geo_kind(const Geo& g) {
+    if (g.WL != 32) return 0;
+    if (g.TH == 32 && g.TW == 128) return 1;
+    if (g.TH == 16 && g.TW == 64) return 2;
+    return 0;
+}
+
 // INIM_ZREV=0: every batched kernel walks the plots in launch order.  Otherwise the
 // vertical pass and the move walk them backwards, so each consumer starts on the plots
 // its producer wrote last (still in L2): h up, v down, write up, move down.

@@ -7,23 +7,6 @@
 
 namespace inim {
 
-// The run tile geometries as compile-time constants of a local Geo (GEO 1: 32 x 128
-// tiles, 2: 16 x 64 tiles, 0: as passed), so the index arithmetic of the scans folds.
-template <int GEO>
-__device__ __forceinline__ Geo fixed_geo(const Geo& g) {
-    Geo f = g;
-    if (GEO == 1) { f.TH = 32; f.TW = 128; f.twlog = 7; f.CPL = 4; f.WL = 32; }
-    if (GEO == 2) { f.TH = 16; f.TW = 64; f.twlog = 6; f.CPL = 2; f.WL = 32; }
-    return f;
-}
-
-inline int geo_kind(const Geo& g) {
-    if (g.WL != 32) return 0;
-    if (g.TH == 32 && g.TW == 128) return 1;
-    if (g.TH == 16 && g.TW == 64) return 2;
-    return 0;
-}
-
 // Launch bounds: the plain 512-thread bound settles at 40 registers (3 CTAs/SM),
 // measured best (an explicit minimum of 1 CTA/SM lets ptxas spend 72
 // registers and costs 4% of the 16384^2 integral pass; 4 CTAs/SM spill).  BATCH: the
