@@ -299,7 +299,7 @@ INIM_DEV int64_t flat_dsuf_count(int dl, int s) {  // #{i' - j' >= dl}
 // two ahead into registers; otherwise `src` is a staged (shared-memory) tile.
 // GEO: the run geometry as compile-time constants (TW = 32 CPL with every lane holding
 // columns, TH = 32 for CPL = 4, 16 for CPL = 2), so the row sweep and the per-row lane
-// tests fold; the caller checks the geometry (and uses it for the 16 x 64 tiles only).
+// tests fold; the caller checks the geometry.
 template <int CPL, int MODE, bool GSRC = false, bool GEO = false>
 __device__ __forceinline__ void warp_tile_write(const float* src, int ld, const Geo g, const Ws ws, int b, int x,
                                                 int lane, const WriteOut out) {
