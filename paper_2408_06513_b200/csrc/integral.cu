@@ -286,7 +286,8 @@ static int launch_write_cpl(const float* d, const Geo& g, const Ws& ws, const Wr
     }
     // the 32 x 128 field pass likewise, at 4 CTAs per SM (127 registers, no spills; at the
     // 5-CTA cap of the generic instance it spilled): C4 37.78 -> 37.19 ms, C3 -1.9%
-    if constexpr (CPL == 4 && MODE == 1) {
+    // (the tables pass too: integral 4096^2 3,733 -> 4,095 GB/s, 8192^2 +1%, 16384^2 +-0)
+    if constexpr (CPL == 4 && MODE != 2) {
         if (g.WL == 32 && g.TW == 128 && g.TH == 32) kern = write_kernel<CPL, MODE, true>;
     }
     INIM_CUDA_TRY(launch_pdl(kern, dim3(tile_ctas(g), 1, bt.B), dim3(kWarpsPerCta * 32), 0, st, d, g, ws, out, state,
